@@ -1,0 +1,157 @@
+/*
+ * fgb200 — C ABI of the B200-native Grünwald–Letnikov history stepper.
+ *
+ * Drop-in boundary for the reference hot path
+ *   /root/reference/pkg/src/fracgrid/solver.py:230-265  run(config)
+ *        → step (solver.py:200-227) → history_sum (solver.py:162-197)
+ * plus the helpers that path depends on:
+ *   coefficients.py:76-92  build_table (ψ recursion)
+ *   schedule.py:70-151     full / short / adaptive memory schedules
+ *   grid.py:88-106         five-point stencil (generalised to 1D/3D)
+ *
+ * The reference is pure Python, so there is no C interface to mirror one-for-one;
+ * these entry points are what a ctypes binding inside fracgrid would call (see
+ * INTEGRATION.md).  All pointers marked _dev are CUDA device pointers; `stream`
+ * is a cudaStream_t passed as void* (NULL = legacy default stream).  No torch
+ * types cross this boundary.  Every function returns FG_OK (0) or a negative
+ * FG_ERR_* code; fg_last_error() describes the most recent failure on the
+ * calling thread.
+ */
+#ifndef FGB200_H
+#define FGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGB200_ABI_VERSION 1
+
+#define FG_OK 0
+#define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
+#define FG_ERR_CUDA (-2)        /* CUDA runtime failure                           */
+#define FG_ERR_UNSUPPORTED (-3) /* shape / kind outside what the kernels handle   */
+
+/* "no divergence yet" value of fg_plan.status[0] */
+#define FG_NO_BAD_STEP INT64_MAX
+
+enum fg_memory_kind {  /* schedule.py:198-254 strategy tags */
+    FG_MEM_FULL = 0,      /* "full"                         */
+    FG_MEM_SHORT = 1,     /* "short", horizon floor(L/dt)   */
+    FG_MEM_ADAPTIVE = 2   /* "adaptive", integer base a>=2  */
+};
+
+enum fg_reaction {
+    FG_REACT_LINEAR = 0,     /* u*decay + diffuse*S           (solver.py:215-217) */
+    FG_REACT_SATURATING = 1  /* u + dt*f(u) + diffuse*S, f(u) = -vmax*u/(km+u)    */
+};
+
+/*
+ * Everything one run needs, as plain device pointers and sizes.  The caller
+ * (Python host, or any C program) owns every buffer; the library never allocates
+ * device memory.  Layout in HBM:
+ *   fields   u[2][B][ms]                      fp64, ping-pong by step parity
+ *   history  H[h_slices][B][ms]               fp64, slice t = δ^t = stencil(u^t)
+ *   ψ        psi[B][psi_stride]               fp64, ψ_b(m), m = 0..n_steps
+ * `ms` (member stride) is n_m rounded up to a multiple of 32 elements, so every
+ * member of every slice starts on a 256-byte boundary and is read with 128-bit
+ * loads.  Padding elements are never part of a result.
+ */
+typedef struct fg_plan {
+    int64_t B;            /* members (independent problems)                       */
+    int64_t n_m;          /* points per member = prod(shape)                      */
+    int64_t ms;           /* member stride in elements (multiple of 32, >= n_m)   */
+    int32_t ndim;         /* 1, 2 or 3                                            */
+    int32_t reaction;     /* enum fg_reaction                                     */
+    int64_t shape[3];     /* member shape, C order; unused trailing entries = 1   */
+    int32_t kind;         /* enum fg_memory_kind                                  */
+    int32_t split;        /* 0 = auto; else warps-per-column split of the sum (1,2,4,8) */
+    int64_t base;         /* adaptive base a                                      */
+    const int64_t* horizon_dev;  /* [B] short-memory floor(L/dt_b), host-evaluated */
+    const double* psi_dev;       /* [B][psi_stride]                                */
+    int64_t psi_stride;          /* >= n_steps + 1                                 */
+    const double* decay_dev;     /* [B] 1 - beta*dt_b (host-evaluated)             */
+    const double* diffuse_dev;   /* [B] alpha*dt_b**gamma_b/dx**2 (host-evaluated) */
+    const double* dt_dev;        /* [B]                                            */
+    double vmax, km;             /* saturating reaction parameters                 */
+    double* H_dev;               /* [h_slices][B*ms]                               */
+    int64_t h_slices;            /* history capacity (n_steps + 1)                 */
+    double* u_dev[2];            /* [B*ms] each                                    */
+    int64_t* status_dev;         /* [2]: [0] first non-finite step or FG_NO_BAD_STEP */
+    int32_t step_flags;          /* FG_STEP_* bits                                 */
+    int32_t reserved;
+} fg_plan;
+
+/* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of
+ * recomputing stencil(u^k) (the reference's step() sums whatever the history
+ * holds, solver.py:214). */
+#define FG_STEP_M0_FROM_HISTORY 1
+
+/* ---- library ---------------------------------------------------------------- */
+int fg_abi_version(void);
+/* sizeof(fg_plan) as compiled into the library (binding layout check). */
+int64_t fg_plan_sizeof(void);
+const char* fg_last_error(void);
+/* 0 on success; fills the SM count and compute capability of the current device. */
+int fg_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---- ψ tables: coefficients.py:76-92, bit-exact ------------------------------
+ * out_dev[b*stride + m] = ψ(gamma_dev[b], m) for m = 0..n, one sequential
+ * recursion per member with correctly rounded sub/mul/div (no FMA). */
+int fg_psi_tables(const double* gamma_dev, int64_t B, int64_t n, int64_t stride,
+                  double* out_dev, void* stream);
+
+/* ---- schedules: schedule.py:70-151, bit-exact --------------------------------
+ * Host helper: number of (offset, weight) entries of schedule(k). */
+int fg_schedule_len(int32_t kind, int64_t k, int64_t base, int64_t horizon, int64_t* len);
+/* Device generator: rows i = 0..nk-1 hold schedule(k0 + i); offsets / weights
+ * are int32 [nk][row_cap]; lens_dev[i] receives the full length (entries past
+ * row_cap are dropped). */
+int fg_schedule_expand(int32_t kind, int64_t k0, int64_t nk, int64_t base, int64_t horizon,
+                       int32_t* offsets_dev, int32_t* weights_dev, int64_t row_cap,
+                       int64_t* lens_dev, void* stream);
+
+/* ---- history_sum: solver.py:162-197 -----------------------------------------
+ * out_dev[p] = Σ_j weights[j]*psi[offsets[j]] * H[(k - offsets[j])*slice_stride + p]
+ * for p < n.  Offsets / weights are int64 device arrays of length len (any
+ * valid MemorySchedule).  FMA accumulation: within 1e-10 of the reference, not
+ * bitwise (different reduction order). */
+int fg_history_sum(const double* H_dev, int64_t slice_stride, int64_t n,
+                   const int64_t* offsets_dev, const int64_t* weights_dev, int64_t len,
+                   const double* psi_dev, int64_t psi_len, int64_t k,
+                   double* out_dev, void* stream);
+
+/* ---- stencil: grid.py:88-106 (zero output ring, no /dx²), bit-exact ------------
+ * out = δ(u) for all B members of the plan's shape; u/out are [B*ms]. */
+int fg_stencil(const fg_plan* plan, const double* u_dev, double* out_dev, void* stream);
+
+/* ---- fused step: solver.py:200-227 -------------------------------------------
+ * One kernel: δ^k = stencil(u^k) → H[k]; S = Σ_j c_j H[k-m_j] (schedule and
+ * c_j = w_j ψ_b(m_j) generated on the device); u^{k+1} = update(u^k, S);
+ * boundary pinned to zero; first non-finite step recorded in status_dev[0]
+ * (later steps become no-ops).  Reads u_dev[k&1], writes u_dev[(k+1)&1] and,
+ * if snap_dev != NULL, a copy of u^{k+1} there. */
+int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
+
+/* Steps k0..k1-1 back to back (solver.py:249-256).  snap_steps (host, sorted)
+ * lists `done` step numbers whose field is copied to
+ * snap_pool_dev + i*B*ms for the i-th entry.  flags: FG_RUN_GRAPH captures the
+ * launches into a CUDA graph; FG_RUN_PDL enables programmatic dependent launch. */
+#define FG_RUN_GRAPH 1
+#define FG_RUN_PDL 2
+int fg_run(const fg_plan* plan, int64_t k0, int64_t k1,
+           const int64_t* snap_steps, int64_t n_snap, double* snap_pool_dev,
+           int32_t flags, void* stream);
+
+/* Stream-synchronous read of status_dev[0] (first non-finite step). */
+int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);
+
+/* Launch geometry fg_step would use: CTAs, threads per CTA, split factor. */
+int fg_step_geometry(const fg_plan* plan, int64_t* ctas, int32_t* threads, int32_t* split);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FGB200_H */

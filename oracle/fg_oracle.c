@@ -170,6 +170,13 @@ int fgo_run(const fgo_problem* p, double* u_io, int64_t n_snap, const int64_t* s
     }
     for (int64_t b = 0; b < B; ++b)
         if (fgo_build_table(p->gamma[b], T, tab + b * (T + 1))) return -1;
+    /* first-touch the history in parallel, outside the timed loop (page faults
+       taken inside the loop serialise on the address-space lock) */
+    {
+        const int64_t total = (steps + 1) * N;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < total; i += 512) H[i] = 0.0;
+    }
     memcpy(u, u_io, (size_t)N * sizeof(double));
     for (int64_t b = 0; b < B; ++b) stencil_member(p, u + b * nm, H + b * nm, 0, nm);
     int64_t si = 0;

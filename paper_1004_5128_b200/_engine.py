@@ -1,0 +1,319 @@
+"""Device engine: owns every HBM buffer of one run and drives the fused step kernel.
+
+This is the B200 replacement for the body of ``solver.run``
+(/root/reference/pkg/src/fracgrid/solver.py:230-265).  It is shared by the
+reference-compatible 2D API (:mod:`.solver`) and the n-D / batched extension
+(:mod:`.problem`).  PyTorch is used only as the device allocator and stream
+provider; all arithmetic on the path runs in the kernels of ``libfgb200.so``.
+
+HBM layout:
+    H      [n_steps+1][B][ms]  fp64   δ^t = stencil(u^t), one slice per step
+    u      [2][B][ms]          fp64   ping-pong fields, u^k in slot k & 1
+    psi    [B][n_steps+1]      fp64   ψ_b(m), generated on the device
+    snaps  [n_snap][B][ms]     fp64   snapshot pool written by the step kernel
+``ms`` = points per member rounded up to 32 (256-byte aligned member rows).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import math
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+log = logging.getLogger("fracgrid")
+
+DEFAULT_HISTORY_BYTE_CAP = 4 * 1024**3  # grid.py:13
+_INT64_BIG = 1 << 62
+
+
+class MemoryBudgetError(ValueError):
+    """History storage for the requested run would exceed the byte cap (grid.py:16-17)."""
+
+
+class HistoryCapacityError(ValueError):
+    """An append would exceed the buffer's preallocated step count (grid.py:20-21)."""
+
+
+class DivergenceError(RuntimeError):
+    """A step produced non-finite concentrations (solver.py:38-46)."""
+
+    def __init__(self, step: int, peak: float):
+        super().__init__(f"solution diverged at step {step}: max |u| reached {peak!r}")
+        self.step = step
+        self.peak = peak
+
+
+def default_flags() -> int:
+    env = os.environ.get("FGB200_RUN_FLAGS")
+    if env is not None:
+        return int(env)
+    return _lib.FG_RUN_PDL
+
+
+def round_up(n: int, m: int) -> int:
+    return (n + m - 1) // m * m
+
+
+def strategy_spec(strategy) -> tuple[str, float]:
+    """Duck-type a memory strategy by ``.tag`` (schedule.py:198-257)."""
+    tag = getattr(strategy, "tag", None)
+    if tag == "full":
+        return "full", 0
+    if tag == "short":
+        length = float(strategy.length)
+        if not length > 0 or not math.isfinite(length):
+            raise ValueError(f"short-memory length must be positive and finite, got {length!r}")
+        return "short", length
+    if tag == "adaptive":
+        base = strategy.base
+        if isinstance(base, bool) or int(base) != base or int(base) < 2:
+            raise ValueError(f"adaptive base must be an integer >= 2, got {base!r}")
+        return "adaptive", int(base)
+    raise TypeError(f"not a memory strategy: {strategy!r}")
+
+
+def short_horizon(length: float, dt: float) -> int:
+    """floor(L/dt) exactly as schedule.py:92 evaluates it (then clamped for int64)."""
+    if not dt > 0 or not math.isfinite(dt):
+        raise ValueError(f"dt must be positive and finite, got {dt!r}")
+    return min(int(math.floor(float(length) / float(dt))), _INT64_BIG)
+
+
+def host_scalars(alpha: float, beta: float, gamma: float, dt: float, dx: float) -> tuple[float, float]:
+    """(decay, diffuse) with the reference's Python-float evaluation (solver.py:215-216)."""
+    decay = 1.0 - float(beta) * float(dt)
+    diffuse = float(alpha) * float(dt) ** float(gamma) / float(dx) ** 2
+    return decay, diffuse
+
+
+def snapshot_steps(n_steps: int, cadence: int) -> list[int]:
+    """0, every ``cadence`` steps, and the final step (solver.py:245-256)."""
+    steps = [0]
+    for done in range(cadence, n_steps + 1, cadence):
+        steps.append(done)
+    if steps[-1] != n_steps:
+        steps.append(n_steps)
+    return steps
+
+
+@dataclass
+class Problem:
+    """Normalised run: ``B`` members sharing one field shape (1-3 dims)."""
+
+    u0: np.ndarray            # (B, *shape) float64, boundary ring zero
+    gamma: np.ndarray         # (B,)
+    dt: np.ndarray            # (B,)
+    alpha: float
+    dx: float
+    reaction: tuple           # ("linear", beta) | ("saturating", vmax, km)
+    kind: str                 # full | short | adaptive
+    param: float
+    n_steps: int
+    cadence: int
+    history_byte_cap: int | None = DEFAULT_HISTORY_BYTE_CAP
+
+    @property
+    def batch(self) -> int:
+        return int(self.u0.shape[0])
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        return tuple(int(s) for s in self.u0.shape[1:])
+
+    @property
+    def n_m(self) -> int:
+        return int(np.prod(self.shape))
+
+    def terms(self) -> int:
+        """Σ_k len_k · N over the run — the metric's numerator."""
+        L = _lib.load()
+        out = C.c_int64(0)
+        total = 0
+        for b in range(self.batch if self.kind == "short" else 1):
+            hz = short_horizon(self.param, float(self.dt[b])) if self.kind == "short" else 0
+            base = int(self.param) if self.kind == "adaptive" else 0
+            s = 0
+            for k in range(self.n_steps):
+                _lib.check(L.fg_schedule_len(_lib.MEM_KINDS[self.kind], k, base, hz, C.byref(out)))
+                s += out.value
+            total += s * self.n_m
+        if self.kind != "short":
+            total *= self.batch
+        return total
+
+
+def check_history_budget(p: Problem) -> None:
+    """MemoryBudgetError before any allocation (grid.py:141-146, same formula)."""
+    n, B, shape = int(p.n_steps), p.batch, p.shape
+    needed = (n + 1) * B * p.n_m * 8
+    if p.history_byte_cap is not None and needed > p.history_byte_cap:
+        members = f" x{B} members" if B > 1 else ""
+        raise MemoryBudgetError(
+            f"history of {n + 1} fields of shape {'x'.join(map(str, shape))}{members} needs "
+            f"{needed} bytes, over the cap of {p.history_byte_cap}")
+
+
+class Stepper:
+    """All device state of one run plus the loop driver."""
+
+    def __init__(self, problem: Problem, *, device=None, split: int = 0, flags: int | None = None,
+                 snapshots: bool = True):
+        import torch
+
+        self.torch = torch
+        self.p = problem
+        p = problem
+        B, shape, n = p.batch, p.shape, int(p.n_steps)
+        if not 1 <= len(shape) <= 3:
+            raise ValueError(f"fields must have 1-3 dimensions, got shape {shape}")
+        if any(s < 3 for s in shape):
+            raise ValueError(f"grid must be at least 3 points per axis, got {shape}")
+        self.n_m = p.n_m
+        self.ms = round_up(self.n_m, 32)
+        check_history_budget(p)
+        self.device = device if device is not None else _lib.require_cuda()
+        self.flags = default_flags() if flags is None else int(flags)
+        L = self.L = _lib.load()
+        slice_elems = B * self.ms
+        self.snap_steps = snapshot_steps(n, p.cadence) if snapshots else []
+        pool_slices = max(0, len([s for s in self.snap_steps if s > 0]))
+        dev_bytes = ((n + 1) + 2 + pool_slices) * slice_elems * 8 + B * (n + 1) * 8
+        free, _total = torch.cuda.mem_get_info(self.device)
+        free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
+        if dev_bytes > free:
+            raise MemoryBudgetError(
+                f"device history and fields need {dev_bytes} bytes, only {free} free on {self.device}")
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.H = torch.empty((n + 1, slice_elems), **f64)
+        self.u = torch.zeros((2, slice_elems), **f64)
+        self.psi = torch.empty((B, n + 1), **f64)
+        self.status = torch.full((2,), _lib.FG_NO_BAD_STEP, dtype=torch.int64, device=self.device)
+        beta = float(p.reaction[1]) if p.reaction[0] == "linear" else 0.0
+        scal = [host_scalars(p.alpha, beta, float(p.gamma[b]), float(p.dt[b]), p.dx) for b in range(B)]
+        self.decay = torch.tensor([s[0] for s in scal], **f64)
+        self.diffuse = torch.tensor([s[1] for s in scal], **f64)
+        self.dt = torch.tensor([float(x) for x in p.dt], **f64)
+        gam = torch.tensor([float(x) for x in p.gamma], **f64)
+        hz = [short_horizon(p.param, float(p.dt[b])) if p.kind == "short" else 0 for b in range(B)]
+        self.horizon = torch.tensor(hz, dtype=torch.int64, device=self.device)
+        self.pool = torch.empty((pool_slices, slice_elems), **f64) if pool_slices else None
+        st = _lib.stream_handle()
+        _lib.check(L.fg_psi_tables(gam.data_ptr(), B, n, n + 1, self.psi.data_ptr(), st), "fg_psi_tables")
+        # upload u^0 (padded rows) — the run's host→device input copy
+        u0 = np.zeros((B, self.ms), dtype=np.float64)
+        u0[:, : self.n_m] = np.asarray(p.u0, dtype=np.float64).reshape(B, self.n_m)
+        self.h2d_bytes = u0.nbytes
+        self.u[0].copy_(torch.from_numpy(u0).reshape(-1).pin_memory(), non_blocking=True)
+        self.d2h_bytes = 0
+
+        plan = _lib.FgPlan()
+        plan.B, plan.n_m, plan.ms = B, self.n_m, self.ms
+        plan.ndim = len(shape)
+        plan.reaction = _lib.REACTIONS[p.reaction[0]]
+        for i in range(3):
+            plan.shape[i] = shape[i] if i < len(shape) else 1
+        plan.kind = _lib.MEM_KINDS[p.kind]
+        plan.split = int(split)
+        plan.base = int(p.param) if p.kind == "adaptive" else 0
+        plan.horizon_dev = self.horizon.data_ptr()
+        plan.psi_dev = self.psi.data_ptr()
+        plan.psi_stride = n + 1
+        plan.decay_dev = self.decay.data_ptr()
+        plan.diffuse_dev = self.diffuse.data_ptr()
+        plan.dt_dev = self.dt.data_ptr()
+        if p.reaction[0] == "saturating":
+            plan.vmax, plan.km = float(p.reaction[1]), float(p.reaction[2])
+        plan.H_dev = self.H.data_ptr()
+        plan.h_slices = n + 1
+        plan.u_dev[0] = self.u[0].data_ptr()
+        plan.u_dev[1] = self.u[1].data_ptr()
+        plan.status_dev = self.status.data_ptr()
+        self.plan = plan
+        self.k = 0
+
+    # ---------------------------------------------------------------- driving --
+    def reset(self, u0_dev) -> None:
+        """Rewind to step 0 from a device-resident padded u^0 (benchmark re-runs)."""
+        self.u[0].copy_(u0_dev)
+        self.status.fill_(_lib.FG_NO_BAD_STEP)
+        self.k = 0
+
+    def geometry(self) -> tuple[int, int, int]:
+        ctas, thr, spl = C.c_int64(0), C.c_int32(0), C.c_int32(0)
+        _lib.check(self.L.fg_step_geometry(C.byref(self.plan), C.byref(ctas), C.byref(thr), C.byref(spl)))
+        return ctas.value, thr.value, spl.value
+
+    def advance(self, k1: int, *, flags: int | None = None) -> None:
+        """Launch steps self.k .. k1-1 (asynchronous, stream-ordered)."""
+        k0 = self.k
+        if k1 <= k0:
+            return
+        snaps = [s for s in self.snap_steps if s > 0]
+        arr = (C.c_int64 * max(1, len(snaps)))(*snaps)
+        pool = self.pool.data_ptr() if self.pool is not None else None
+        rc = self.L.fg_run(C.byref(self.plan), k0, k1, arr, len(snaps), pool,
+                           self.flags if flags is None else flags, _lib.stream_handle())
+        _lib.check(rc, "fg_run")
+        self.k = k1
+
+    def run(self, progress_every: int = 0) -> float:
+        """Run every step; return the loop's wall time (solver.py:248-257 semantics)."""
+        torch = self.torch
+        n = int(self.p.n_steps)
+        torch.cuda.synchronize(self.device)
+        t0 = time.perf_counter()
+        if progress_every and progress_every > 0:
+            for stop in list(range(progress_every, n + 1, progress_every)) + [n]:
+                if stop <= self.k:
+                    continue
+                self.advance(stop)
+                torch.cuda.synchronize(self.device)
+                if stop % progress_every == 0:
+                    self.raise_if_diverged()
+                    log.info("step %d/%d", stop, n)
+        else:
+            self.advance(n)
+        torch.cuda.synchronize(self.device)
+        elapsed = time.perf_counter() - t0
+        self.raise_if_diverged()
+        return elapsed
+
+    def first_bad_step(self) -> int | None:
+        v = int(self.status[0].item())
+        return None if v == _lib.FG_NO_BAD_STEP else v
+
+    def raise_if_diverged(self) -> None:
+        bad = self.first_bad_step()
+        if bad is None:
+            return
+        field = self.u[bad & 1].reshape(self.p.batch, self.ms)[:, : self.n_m]
+        fin = field[self.torch.isfinite(field)]
+        peak = float(fin.abs().max().item()) if fin.numel() else math.inf
+        raise DivergenceError(bad, peak)
+
+    # -------------------------------------------------------------- results --
+    def fetch_snapshots(self) -> list[tuple[int, np.ndarray]]:
+        """Device pool → host (one D2H copy); step 0 is the input field itself."""
+        B, shape = self.p.batch, self.p.shape
+        out = [(0, np.array(self.p.u0, dtype=np.float64).reshape((B,) + shape))]
+        later = [s for s in self.snap_steps if s > 0]
+        self.d2h_bytes = 0
+        if later:
+            host = self.pool.to("cpu", non_blocking=False)
+            self.d2h_bytes = host.numel() * 8
+            arr = host.numpy().reshape(len(later), B, self.ms)[:, :, : self.n_m]
+            for i, s in enumerate(later):
+                out.append((s, arr[i].reshape((B,) + shape).copy()))
+        return out
+
+    def field(self, k: int | None = None) -> np.ndarray:
+        k = self.k if k is None else k
+        arr = self.u[k & 1].reshape(self.p.batch, self.ms)[:, : self.n_m].cpu().numpy()
+        return arr.reshape((self.p.batch,) + self.p.shape)

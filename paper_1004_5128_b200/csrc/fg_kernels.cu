@@ -1,0 +1,644 @@
+// B200 (sm_100a) kernels and the C ABI of the GL history stepper.
+//
+// Hot path replaced: /root/reference/pkg/src/fracgrid/solver.py:230-265 (run)
+//   → step (:200-227) → history_sum (:162-197), with ψ from coefficients.py:76-92,
+//   schedules from schedule.py:70-151 and the stencil of grid.py:88-106.
+//
+// Design:
+//  * fg_step_kernel — ONE kernel per time step.  A CTA owns a tile of TP points of
+//    one member.  Prologue: δ^k = stencil(u^k) for the tile (the m = 0 term, kept
+//    in registers and stored to H[k]).  Body: the schedule of step k is generated
+//    in shared memory (segment table → (slice index, coefficient) pairs, with
+//    c_j = w_j·ψ_b(m_j) rounded once exactly like solver.py:190), then the
+//    selected history slices are streamed with 128-bit non-allocating loads, 8
+//    slices in flight per thread, FMA-accumulated in fp64 registers.  When a tile
+//    is small the CTA's warps split the slice list S ways and combine the
+//    partial sums in a fixed order through shared memory (deterministic).
+//    Epilogue: reaction + explicit update with the reference's rounding order,
+//    boundary ring pinned to zero, non-finite detection (atomicMin of the step
+//    number), u^{k+1} (and optionally a snapshot copy) stored.
+//  * The path is HBM-bound (0.25 flop/B): no tensor cores; the roofline is
+//    8 bytes per history term.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/fgb200.h"
+#include "fg_schedule.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return FG_OK;
+    return fail(FG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr int kThreads = 256;   // 8 warps
+constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit load)
+constexpr int kUnroll = 8;      // slices in flight per thread
+constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
+
+// ---------------------------------------------------------------- PTX helpers ---
+
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void st_pair(double* p, double a, double b) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+// ------------------------------------------------------------------- stencil ---
+// grid.py:98-105 operation order, each op correctly rounded (no contraction):
+//   2D ((((x+ + x-) - 4c) + y+) + y-); 1D (x+ + x-) - 2c; 3D with -6c, y±, z±.
+
+struct Shape {
+    int32_t n0, n1, n2;  // C-order extents (unused = 1)
+};
+
+template <int NDIM>
+__device__ __forceinline__ bool interior(const Shape& sh, int32_t q) {
+    if (NDIM == 1) return q > 0 && q < sh.n0 - 1;
+    if (NDIM == 2) {
+        const int32_t j = q / sh.n1, l = q - j * sh.n1;
+        return j > 0 && j < sh.n0 - 1 && l > 0 && l < sh.n1 - 1;
+    }
+    const int32_t plane = sh.n1 * sh.n2;
+    const int32_t i0 = q / plane, r = q - i0 * plane;
+    const int32_t i1 = r / sh.n2, i2 = r - i1 * sh.n2;
+    return i0 > 0 && i0 < sh.n0 - 1 && i1 > 0 && i1 < sh.n1 - 1 && i2 > 0 && i2 < sh.n2 - 1;
+}
+
+template <int NDIM>
+__device__ __forceinline__ double delta_at(const double* __restrict__ u, const Shape& sh, int32_t q,
+                                           double c) {
+    if (!interior<NDIM>(sh, q)) return 0.0;
+    if (NDIM == 1) {
+        return __dsub_rn(__dadd_rn(__ldg(u + q + 1), __ldg(u + q - 1)), __dmul_rn(2.0, c));
+    } else if (NDIM == 2) {
+        const int32_t sx = sh.n1;
+        double r = __dadd_rn(__ldg(u + q + sx), __ldg(u + q - sx));
+        r = __dsub_rn(r, __dmul_rn(4.0, c));
+        r = __dadd_rn(r, __ldg(u + q + 1));
+        return __dadd_rn(r, __ldg(u + q - 1));
+    } else {
+        const int32_t sy = sh.n2, sx = sh.n1 * sh.n2;
+        double r = __dadd_rn(__ldg(u + q + sx), __ldg(u + q - sx));
+        r = __dsub_rn(r, __dmul_rn(6.0, c));
+        r = __dadd_rn(r, __ldg(u + q + sy));
+        r = __dadd_rn(r, __ldg(u + q - sy));
+        r = __dadd_rn(r, __ldg(u + q + 1));
+        return __dadd_rn(r, __ldg(u + q - 1));
+    }
+}
+
+// ---------------------------------------------------------------- fused step ---
+
+struct StepArgs {
+    const double* u_in;
+    double* u_out;
+    double* snap;          // nullable
+    double* H;
+    const double* psi;
+    const double* decay;
+    const double* diffuse;
+    const double* dt;
+    const int64_t* horizon;
+    int64_t* status;
+    int64_t k;
+    int64_t slice_stride;  // B*ms
+    int64_t ms;
+    int64_t psi_stride;
+    int64_t base;
+    double vmax, km;
+    Shape sh;
+    int32_t n_m;
+    int32_t kind;
+    int32_t tiles_per_member;
+    int32_t pdl;
+    int32_t m0_from_history;
+};
+
+template <int NDIM, int REACT, int S>
+__global__ void __launch_bounds__(kThreads, 2) fg_step_kernel(const StepArgs a) {
+    constexpr int kCols = (kThreads / 32) / S;   // warps across the tile
+    constexpr int TP = kCols * 32 * kVec;        // points per tile
+    __shared__ FgSeg segs[FG_MAX_SEGS];
+    __shared__ int64_t seg_first[FG_MAX_SEGS + 1];
+    __shared__ int s_nseg;
+    __shared__ int32_t s_t[kChunk];
+    __shared__ double s_c[kChunk];
+    __shared__ double2 s_part[S > 1 ? (S - 1) * kCols * 32 : 1];
+
+    if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (*(volatile const int64_t*)a.status != FG_NO_BAD_STEP) return;  // diverged earlier
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int col = warp % kCols, split = warp / kCols;
+    const int64_t b = blockIdx.y;
+    const int32_t q = (int32_t)blockIdx.x * TP + col * 64 + lane * kVec;
+    const bool active = q < a.n_m;
+    const int64_t k = a.k;
+    const double* psi_b = a.psi + b * a.psi_stride;
+    const int64_t moff = b * a.ms + q;
+
+    // schedule of step k as segments (thread 0), prefix of entry counts
+    if (tid == 0) {
+        const int64_t hz = a.kind == 1 ? a.horizon[b] : 0;
+        int n = fg_segments(a.kind, k, a.base, hz, segs);
+        int64_t acc = 0;
+        for (int i = 0; i < n; ++i) {
+            seg_first[i] = acc;
+            acc += segs[i].count;
+        }
+        seg_first[n] = acc;
+        s_nseg = n;
+    }
+
+    // prologue (split 0): δ^k = stencil(u^k) → H[k], the m = 0 term
+    double u0 = 0.0, u1 = 0.0, acc0 = 0.0, acc1 = 0.0;
+    if (split == 0 && active) {
+        const double* ub = a.u_in + b * a.ms;
+        const double2 uu = *reinterpret_cast<const double2*>(ub + q);
+        u0 = uu.x;
+        u1 = uu.y;
+        double d0, d1;
+        if (a.m0_from_history) {
+            const double2 h = *reinterpret_cast<const double2*>(a.H + k * a.slice_stride + moff);
+            d0 = h.x;
+            d1 = h.y;
+        } else {
+            d0 = delta_at<NDIM>(ub, a.sh, q, u0);
+            d1 = (q + 1 < a.n_m) ? delta_at<NDIM>(ub, a.sh, q + 1, u1) : 0.0;
+            st_pair(a.H + k * a.slice_stride + moff, d0, d1);
+        }
+        const double c0 = psi_b[0];  // w_0 * ψ(0) = 1 * 1
+        acc0 = __dmul_rn(c0, d0);
+        acc1 = __dmul_rn(c0, d1);
+    }
+    __syncthreads();
+
+    const int nseg = s_nseg;
+    const int64_t len = seg_first[nseg];
+    const double* hbase = a.H + moff;
+    // entries j = 1..len-1 (j = 0 is m = 0, done above), staged kChunk at a time
+    for (int64_t c0 = 1; c0 < len; c0 += kChunk) {
+        const int cn = (int)((len - c0) < kChunk ? (len - c0) : kChunk);
+        for (int e = tid; e < cn; e += kThreads) {
+            const int64_t j = c0 + e;
+            int si = 0;
+            while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
+            const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
+            s_t[e] = (int32_t)(k - m);
+            s_c[e] = __dmul_rn((double)segs[si].stride, psi_b[m]);
+        }
+        __syncthreads();
+        if (active) {
+            for (int e0 = split; e0 < cn; e0 += S * kUnroll) {
+                double2 v[kUnroll];
+                double c[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int e = e0 + u * S;
+                    if (e < cn) {
+                        v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
+                        c[u] = s_c[e];
+                    } else {
+                        v[u] = make_double2(0.0, 0.0);
+                        c[u] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    acc0 = fma(c[u], v[u].x, acc0);
+                    acc1 = fma(c[u], v[u].y, acc1);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    if (S > 1) {
+        if (split > 0) s_part[((split - 1) * kCols + col) * 32 + lane] = make_double2(acc0, acc1);
+        __syncthreads();
+        if (split == 0) {
+#pragma unroll
+            for (int s = 1; s < S; ++s) {
+                const double2 p = s_part[((s - 1) * kCols + col) * 32 + lane];
+                acc0 = __dadd_rn(acc0, p.x);
+                acc1 = __dadd_rn(acc1, p.y);
+            }
+        }
+    }
+    if (split != 0 || !active) return;
+    if (a.pdl) asm volatile("griddepcontrol.launch_dependents;");
+
+    // epilogue: solver.py:215-226 rounding order, ring pinned, non-finite check
+    const double diffuse = a.diffuse[b];
+    double n0, n1;
+    if (REACT == 0) {
+        const double decay = a.decay[b];
+        n0 = __dadd_rn(__dmul_rn(u0, decay), __dmul_rn(diffuse, acc0));
+        n1 = __dadd_rn(__dmul_rn(u1, decay), __dmul_rn(diffuse, acc1));
+    } else {
+        const double dt = a.dt[b];
+        const double f0 = __ddiv_rn(__dmul_rn(-a.vmax, u0), __dadd_rn(a.km, u0));
+        const double f1 = __ddiv_rn(__dmul_rn(-a.vmax, u1), __dadd_rn(a.km, u1));
+        n0 = __dadd_rn(__dadd_rn(u0, __dmul_rn(dt, f0)), __dmul_rn(diffuse, acc0));
+        n1 = __dadd_rn(__dadd_rn(u1, __dmul_rn(dt, f1)), __dmul_rn(diffuse, acc1));
+    }
+    if (!interior<NDIM>(a.sh, q)) n0 = 0.0;
+    if (q + 1 >= a.n_m || !interior<NDIM>(a.sh, q + 1)) n1 = 0.0;
+    if (!isfinite(n0) || !isfinite(n1))
+        atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
+    st_pair(a.u_out + moff, n0, n1);
+    if (a.snap) st_pair(a.snap + moff, n0, n1);
+}
+
+// ------------------------------------------------------------------ ψ tables ---
+// coefficients.py:86-91: v = ((-v) * ((2 - γ) - m)) / m, each op rounded once.
+__global__ void fg_psi_kernel(const double* __restrict__ gamma, int64_t B, int64_t n, int64_t stride,
+                              double* __restrict__ out) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double g = gamma[b];
+    const double two_minus_g = __dsub_rn(2.0, g);
+    double* o = out + b * stride;
+    double v = 1.0;
+    o[0] = v;
+    for (int64_t m = 1; m <= n; ++m) {
+        const double fm = (double)m;
+        v = __ddiv_rn(__dmul_rn(-v, __dsub_rn(two_minus_g, fm)), fm);
+        o[m] = v;
+    }
+}
+
+// ----------------------------------------------------------- schedule expand ---
+__global__ void fg_schedule_kernel(int kind, int64_t k0, int64_t base, int64_t horizon, int32_t* offs,
+                                   int32_t* wts, int64_t row_cap, int64_t* lens) {
+    __shared__ FgSeg segs[FG_MAX_SEGS];
+    __shared__ int64_t first[FG_MAX_SEGS + 1];
+    __shared__ int s_n;
+    const int64_t k = k0 + blockIdx.x;
+    if (threadIdx.x == 0) {
+        int n = fg_segments(kind, k, base, horizon, segs);
+        int64_t acc = 0;
+        for (int i = 0; i < n; ++i) {
+            first[i] = acc;
+            acc += segs[i].count;
+        }
+        first[n > 0 ? n : 0] = acc;
+        s_n = n;
+        lens[blockIdx.x] = n > 0 ? acc : -1;
+    }
+    __syncthreads();
+    const int n = s_n;
+    if (n <= 0) return;
+    const int64_t len = first[n];
+    const int64_t lim = len < row_cap ? len : row_cap;
+    int32_t* orow = offs + (int64_t)blockIdx.x * row_cap;
+    int32_t* wrow = wts + (int64_t)blockIdx.x * row_cap;
+    for (int64_t j = threadIdx.x; j < lim; j += blockDim.x) {
+        int si = 0;
+        while (si + 1 < n && first[si + 1] <= j) ++si;
+        orow[j] = (int32_t)(segs[si].m0 + (j - first[si]) * segs[si].stride);
+        wrow[j] = (int32_t)segs[si].stride;
+    }
+}
+
+// -------------------------------------------------------- generic history_sum ---
+__global__ void fg_history_sum_kernel(const double* __restrict__ H, int64_t ss, int64_t n,
+                                      const int64_t* __restrict__ offs, const int64_t* __restrict__ wts,
+                                      int64_t len, const double* __restrict__ psi, int64_t k,
+                                      double* __restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    double acc = 0.0;
+    for (int64_t j = 0; j < len; ++j) {
+        const int64_t m = offs[j];
+        const double c = __dmul_rn((double)wts[j], psi[m]);
+        acc = fma(c, H[(k - m) * ss + p], acc);
+    }
+    out[p] = acc;
+}
+
+// ------------------------------------------------------------ plain stencil ---
+template <int NDIM>
+__global__ void fg_stencil_kernel(const double* __restrict__ u, double* __restrict__ out, int64_t B,
+                                  int64_t ms, int32_t n_m, Shape sh) {
+    const int64_t b = blockIdx.y;
+    const int32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_m) return;
+    const double* ub = u + b * ms;
+    out[b * ms + q] = delta_at<NDIM>(ub, sh, q, ub[q]);
+}
+
+// ------------------------------------------------------------------ host side ---
+
+int validate_plan(const fg_plan* p) {
+    if (!p) return fail(FG_ERR_ARG, "plan is NULL");
+    if (p->ndim < 1 || p->ndim > 3) return fail(FG_ERR_UNSUPPORTED, "ndim must be 1..3, got %d", p->ndim);
+    if (p->B < 1 || p->B > 65535) return fail(FG_ERR_UNSUPPORTED, "members B must be 1..65535");
+    if (p->n_m < 3 || p->n_m > (int64_t)1 << 30) return fail(FG_ERR_UNSUPPORTED, "points per member out of range");
+    if (p->ms < p->n_m || p->ms % 32) return fail(FG_ERR_ARG, "member stride must be >= n_m and a multiple of 32");
+    int64_t prod = 1;
+    for (int i = 0; i < p->ndim; ++i) {
+        if (p->shape[i] < 3) return fail(FG_ERR_ARG, "every extent must be >= 3");
+        prod *= p->shape[i];
+    }
+    if (prod != p->n_m) return fail(FG_ERR_ARG, "prod(shape) != n_m");
+    if (p->kind < 0 || p->kind > 2) return fail(FG_ERR_ARG, "unknown memory kind %d", p->kind);
+    if (p->kind == 2 && p->base < 2) return fail(FG_ERR_ARG, "adaptive base must be >= 2");
+    if (p->kind == 1 && !p->horizon_dev) return fail(FG_ERR_ARG, "short memory needs horizon_dev");
+    if (p->reaction < 0 || p->reaction > 1) return fail(FG_ERR_ARG, "unknown reaction %d", p->reaction);
+    if (!p->psi_dev || !p->H_dev || !p->u_dev[0] || !p->u_dev[1] || !p->status_dev || !p->decay_dev ||
+        !p->diffuse_dev || !p->dt_dev)
+        return fail(FG_ERR_ARG, "plan has a NULL device pointer");
+    if (p->split != 0 && p->split != 1 && p->split != 2 && p->split != 4 && p->split != 8)
+        return fail(FG_ERR_ARG, "split must be 0, 1, 2, 4 or 8");
+    return FG_OK;
+}
+
+Shape shape_of(const fg_plan* p) {
+    Shape s;
+    s.n0 = (int32_t)p->shape[0];
+    s.n1 = p->ndim >= 2 ? (int32_t)p->shape[1] : 1;
+    s.n2 = p->ndim >= 3 ? (int32_t)p->shape[2] : 1;
+    return s;
+}
+
+int g_sm_count = 0;
+
+int sm_count() {
+    if (g_sm_count == 0) {
+        int dev = 0, n = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            g_sm_count = n;
+        else
+            g_sm_count = 148;
+    }
+    return g_sm_count;
+}
+
+// Pick the split factor: the smallest S whose CTA count reaches two CTAs per SM.
+int choose_split(const fg_plan* p) {
+    if (p->split) return p->split;
+    const int64_t want = 2LL * sm_count();
+    for (int s = 1; s <= 8; s *= 2) {
+        const int64_t tp = (int64_t)((kThreads / 32) / s) * 32 * kVec;
+        const int64_t ctas = ((p->n_m + tp - 1) / tp) * p->B;
+        if (ctas >= want) return s;
+    }
+    return 8;
+}
+
+int64_t tile_points(int s) { return (int64_t)((kThreads / 32) / s) * 32 * kVec; }
+
+typedef void (*StepKernel)(const StepArgs);
+
+template <int NDIM, int REACT>
+StepKernel pick_s(int s) {
+    switch (s) {
+        case 1: return fg_step_kernel<NDIM, REACT, 1>;
+        case 2: return fg_step_kernel<NDIM, REACT, 2>;
+        case 4: return fg_step_kernel<NDIM, REACT, 4>;
+        default: return fg_step_kernel<NDIM, REACT, 8>;
+    }
+}
+
+StepKernel pick_kernel(int ndim, int react, int s) {
+    if (ndim == 1) return react ? pick_s<1, 1>(s) : pick_s<1, 0>(s);
+    if (ndim == 2) return react ? pick_s<2, 1>(s) : pick_s<2, 0>(s);
+    return react ? pick_s<3, 1>(s) : pick_s<3, 0>(s);
+}
+
+StepArgs make_args(const fg_plan* p, int64_t k, double* snap, int pdl) {
+    StepArgs a;
+    a.u_in = p->u_dev[k & 1];
+    a.u_out = p->u_dev[(k + 1) & 1];
+    a.snap = snap;
+    a.H = p->H_dev;
+    a.psi = p->psi_dev;
+    a.decay = p->decay_dev;
+    a.diffuse = p->diffuse_dev;
+    a.dt = p->dt_dev;
+    a.horizon = p->horizon_dev;
+    a.status = p->status_dev;
+    a.k = k;
+    a.slice_stride = p->B * p->ms;
+    a.ms = p->ms;
+    a.psi_stride = p->psi_stride;
+    a.base = p->base;
+    a.vmax = p->vmax;
+    a.km = p->km;
+    a.sh = shape_of(p);
+    a.n_m = (int32_t)p->n_m;
+    a.kind = p->kind;
+    a.pdl = pdl;
+    a.m0_from_history = (p->step_flags & FG_STEP_M0_FROM_HISTORY) ? 1 : 0;
+    return a;
+}
+
+int launch_step(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, int pdl) {
+    const int s = choose_split(p);
+    const int64_t tp = tile_points(s);
+    StepArgs a = make_args(p, k, snap, pdl);
+    a.tiles_per_member = (int32_t)((p->n_m + tp - 1) / tp);
+    StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.tiles_per_member, (unsigned)p->B, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (pdl) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step launch");
+}
+
+}  // namespace
+
+// ================================================================== C ABI =====
+
+extern "C" {
+
+int fg_abi_version(void) { return FGB200_ABI_VERSION; }
+
+int64_t fg_plan_sizeof(void) { return (int64_t)sizeof(fg_plan); }
+
+const char* fg_last_error(void) { return g_last_error.c_str(); }
+
+int fg_device_info(int32_t* sm, int32_t* major, int32_t* minor) {
+    int dev = 0;
+    if (int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+    int v = 0;
+    if (sm) {
+        if (int rc = cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev), "attr")) return rc;
+        *sm = v;
+    }
+    if (major) {
+        if (int rc = cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev), "attr")) return rc;
+        *major = v;
+    }
+    if (minor) {
+        if (int rc = cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev), "attr")) return rc;
+        *minor = v;
+    }
+    return FG_OK;
+}
+
+int fg_psi_tables(const double* gamma_dev, int64_t B, int64_t n, int64_t stride, double* out_dev, void* stream) {
+    if (!gamma_dev || !out_dev || B < 1 || n < 0 || stride < n + 1)
+        return fail(FG_ERR_ARG, "fg_psi_tables: bad arguments");
+    const int threads = 128;
+    fg_psi_kernel<<<(unsigned)((B + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+        gamma_dev, B, n, stride, out_dev);
+    return cuda_check(cudaGetLastError(), "fg_psi_kernel");
+}
+
+int fg_schedule_len(int32_t kind, int64_t k, int64_t base, int64_t horizon, int64_t* len) {
+    FgSeg s[FG_MAX_SEGS];
+    int n = fg_segments(kind, k, base, horizon, s);
+    if (n < 0) return fail(FG_ERR_ARG, "fg_schedule_len: invalid schedule arguments");
+    if (len) *len = fg_schedule_length(s, n);
+    return FG_OK;
+}
+
+int fg_schedule_expand(int32_t kind, int64_t k0, int64_t nk, int64_t base, int64_t horizon, int32_t* offs,
+                       int32_t* wts, int64_t row_cap, int64_t* lens, void* stream) {
+    if (!offs || !wts || !lens || nk < 1 || row_cap < 1 || k0 < 0 || nk > 0x7fffffff)
+        return fail(FG_ERR_ARG, "fg_schedule_expand: bad arguments");
+    FgSeg s[FG_MAX_SEGS];
+    if (fg_segments(kind, k0, base, horizon, s) < 0) return fail(FG_ERR_ARG, "fg_schedule_expand: invalid schedule");
+    fg_schedule_kernel<<<(unsigned)nk, 128, 0, (cudaStream_t)stream>>>(kind, k0, base, horizon, offs, wts,
+                                                                        row_cap, lens);
+    return cuda_check(cudaGetLastError(), "fg_schedule_kernel");
+}
+
+int fg_history_sum(const double* H, int64_t ss, int64_t n, const int64_t* offs, const int64_t* wts,
+                   int64_t len, const double* psi, int64_t psi_len, int64_t k, double* out, void* stream) {
+    if (!H || !offs || !wts || !psi || !out || n < 1 || len < 1 || k < 0 || ss < n)
+        return fail(FG_ERR_ARG, "fg_history_sum: bad arguments");
+    (void)psi_len;  // bounds are validated by the host before the call (solver.py:177-189)
+    const int threads = 256;
+    fg_history_sum_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+        H, ss, n, offs, wts, len, psi, k, out);
+    return cuda_check(cudaGetLastError(), "fg_history_sum_kernel");
+}
+
+int fg_stencil(const fg_plan* p, const double* u, double* out, void* stream) {
+    if (int rc = validate_plan(p)) return rc;
+    if (!u || !out) return fail(FG_ERR_ARG, "fg_stencil: NULL field");
+    const int threads = 256;
+    dim3 grid((unsigned)((p->n_m + threads - 1) / threads), (unsigned)p->B);
+    const Shape sh = shape_of(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->ndim == 1)
+        fg_stencil_kernel<1><<<grid, threads, 0, st>>>(u, out, p->B, p->ms, (int32_t)p->n_m, sh);
+    else if (p->ndim == 2)
+        fg_stencil_kernel<2><<<grid, threads, 0, st>>>(u, out, p->B, p->ms, (int32_t)p->n_m, sh);
+    else
+        fg_stencil_kernel<3><<<grid, threads, 0, st>>>(u, out, p->B, p->ms, (int32_t)p->n_m, sh);
+    return cuda_check(cudaGetLastError(), "fg_stencil_kernel");
+}
+
+int fg_step(const fg_plan* p, int64_t k, double* snap, void* stream) {
+    if (int rc = validate_plan(p)) return rc;
+    if (k < 0 || k + 1 >= p->h_slices + 1 || k >= p->psi_stride) return fail(FG_ERR_ARG, "fg_step: k out of range");
+    return launch_step(p, k, snap, (cudaStream_t)stream, 0);
+}
+
+int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, int64_t n_snap, double* pool,
+           int32_t flags, void* stream) {
+    if (int rc = validate_plan(p)) return rc;
+    if (k0 < 0 || k1 < k0 || k1 > p->h_slices || k1 > p->psi_stride)
+        return fail(FG_ERR_ARG, "fg_run: step range [%lld, %lld) outside history capacity %lld", (long long)k0,
+                    (long long)k1, (long long)p->h_slices);
+    if (n_snap > 0 && (!snap_steps || !pool)) return fail(FG_ERR_ARG, "fg_run: snapshots need steps and a pool");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int pdl = (flags & FG_RUN_PDL) ? 1 : 0;
+    const bool graph = (flags & FG_RUN_GRAPH) != 0;
+    const int64_t slice = p->B * p->ms;
+    cudaStream_t cap = st;
+    cudaGraph_t g = nullptr;
+    if (graph) {
+        if (int rc = cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture"))
+            return rc;
+    }
+    int64_t si = 0;
+    while (si < n_snap && snap_steps[si] <= k0) ++si;
+    int rc = FG_OK;
+    for (int64_t k = k0; k < k1 && rc == FG_OK; ++k) {
+        double* snap = nullptr;
+        if (si < n_snap && snap_steps[si] == k + 1) {
+            snap = pool + si * slice;
+            ++si;
+        }
+        rc = launch_step(p, k, snap, cap, pdl && k > k0);
+    }
+    if (graph) {
+        cudaError_t e = cudaStreamEndCapture(cap, &g);
+        if (rc != FG_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (int r2 = cuda_check(e, "end capture")) return r2;
+        cudaGraphExec_t ge = nullptr;
+        if (int r2 = cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate")) {
+            cudaGraphDestroy(g);
+            return r2;
+        }
+        rc = cuda_check(cudaGraphLaunch(ge, st), "graph launch");
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+    }
+    return rc;
+}
+
+int fg_status(const fg_plan* p, int64_t* first_bad, void* stream) {
+    if (!p || !p->status_dev || !first_bad) return fail(FG_ERR_ARG, "fg_status: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = cuda_check(cudaMemcpyAsync(first_bad, p->status_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+                            "status copy"))
+        return rc;
+    return cuda_check(cudaStreamSynchronize(st), "status sync");
+}
+
+int fg_step_geometry(const fg_plan* p, int64_t* ctas, int32_t* threads, int32_t* split) {
+    if (int rc = validate_plan(p)) return rc;
+    const int s = choose_split(p);
+    const int64_t tp = tile_points(s);
+    if (ctas) *ctas = ((p->n_m + tp - 1) / tp) * p->B;
+    if (threads) *threads = kThreads;
+    if (split) *split = s;
+    return FG_OK;
+}
+
+}  // extern "C"
