@@ -78,9 +78,13 @@ typedef struct fg_plan {
     double* H_dev;               /* [h_slices][B*ms]                               */
     int64_t h_slices;            /* history capacity (n_steps + 1)                 */
     double* u_dev[2];            /* [B*ms] each                                    */
-    int64_t* status_dev;         /* [2]: [0] first non-finite step or FG_NO_BAD_STEP */
+    int64_t* status_dev;         /* [2]: [0] first non-finite step or FG_NO_BAD_STEP,
+                                    [1] grid-barrier counter (library scratch)     */
     int32_t step_flags;          /* FG_STEP_* bits                                 */
     int32_t reserved;
+    int32_t* snap_slot_dev;      /* [h_slices+1] scratch for FG_RUN_PERSISTENT snapshots
+                                    (filled by fg_run; NULL if no snapshots)       */
+    int64_t horizon_max;         /* host copy of max(horizon_dev) (0 = unknown)    */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of
@@ -134,12 +138,19 @@ int fg_stencil(const fg_plan* plan, const double* u_dev, double* out_dev, void* 
  * if snap_dev != NULL, a copy of u^{k+1} there. */
 int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
 
-/* Steps k0..k1-1 back to back (solver.py:249-256).  snap_steps (host, sorted)
- * lists `done` step numbers whose field is copied to
- * snap_pool_dev + i*B*ms for the i-th entry.  flags: FG_RUN_GRAPH captures the
- * launches into a CUDA graph; FG_RUN_PDL enables programmatic dependent launch. */
+/* Steps k0..k1-1 (solver.py:249-256).  snap_steps (host, sorted) lists `done`
+ * step numbers whose field is copied to snap_pool_dev + i*B*ms for the i-th
+ * entry.  flags:
+ *   FG_RUN_PERSISTENT  one cooperative launch runs every step; CTAs own fixed
+ *                      tiles and meet at a split arrive/wait grid barrier once
+ *                      per step (falls back to per-step launches if the grid
+ *                      cannot be co-resident);
+ *   FG_RUN_PDL         per-step launches with programmatic dependent launch;
+ *   FG_RUN_GRAPH       per-step launches captured into one CUDA graph.
+ * All modes produce bitwise-identical results. */
 #define FG_RUN_GRAPH 1
 #define FG_RUN_PDL 2
+#define FG_RUN_PERSISTENT 4
 int fg_run(const fg_plan* plan, int64_t k0, int64_t k1,
            const int64_t* snap_steps, int64_t n_snap, double* snap_pool_dev,
            int32_t flags, void* stream);

@@ -54,6 +54,8 @@ def default_flags() -> int:
     env = os.environ.get("FGB200_RUN_FLAGS")
     if env is not None:
         return int(env)
+    # per-step launches chained with programmatic dependent launch measured
+    # fastest on B200 (profiles/): the next step's A phase fills this step's tail
     return _lib.FG_RUN_PDL
 
 
@@ -204,6 +206,7 @@ class Stepper:
         hz = [short_horizon(p.param, float(p.dt[b])) if p.kind == "short" else 0 for b in range(B)]
         self.horizon = torch.tensor(hz, dtype=torch.int64, device=self.device)
         self.pool = torch.empty((pool_slices, slice_elems), **f64) if pool_slices else None
+        self.snap_slot = torch.empty((n + 2,), dtype=torch.int32, device=self.device) if pool_slices else None
         st = _lib.stream_handle()
         _lib.check(L.fg_psi_tables(gam.data_ptr(), B, n, n + 1, self.psi.data_ptr(), st), "fg_psi_tables")
         # upload u^0 (padded rows) — the run's host→device input copy
@@ -235,6 +238,8 @@ class Stepper:
         plan.u_dev[0] = self.u[0].data_ptr()
         plan.u_dev[1] = self.u[1].data_ptr()
         plan.status_dev = self.status.data_ptr()
+        plan.snap_slot_dev = self.snap_slot.data_ptr() if self.snap_slot is not None else None
+        plan.horizon_max = max(hz) if p.kind == "short" else 0
         self.plan = plan
         self.k = 0
 

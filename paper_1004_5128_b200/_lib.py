@@ -19,6 +19,7 @@ FG_ERR_UNSUPPORTED = -3
 FG_NO_BAD_STEP = (1 << 63) - 1
 FG_RUN_GRAPH = 1
 FG_RUN_PDL = 2
+FG_RUN_PERSISTENT = 4
 FG_STEP_M0_FROM_HISTORY = 1
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
@@ -63,6 +64,8 @@ class FgPlan(C.Structure):
         ("status_dev", C.c_void_p),
         ("step_flags", C.c_int32),
         ("reserved", C.c_int32),
+        ("snap_slot_dev", C.c_void_p),
+        ("horizon_max", C.c_int64),
     ]
 
 

@@ -5,20 +5,25 @@
 //   schedules from schedule.py:70-151 and the stencil of grid.py:88-106.
 //
 // Design:
-//  * fg_step_kernel — ONE kernel per time step.  A CTA owns a tile of TP points of
-//    one member.  Prologue: δ^k = stencil(u^k) for the tile (the m = 0 term, kept
-//    in registers and stored to H[k]).  Body: the schedule of step k is generated
-//    in shared memory (segment table → (slice index, coefficient) pairs, with
-//    c_j = w_j·ψ_b(m_j) rounded once exactly like solver.py:190), then the
-//    selected history slices are streamed with 128-bit non-allocating loads, 8
-//    slices in flight per thread, FMA-accumulated in fp64 registers.  When a tile
-//    is small the CTA's warps split the slice list S ways and combine the
-//    partial sums in a fixed order through shared memory (deterministic).
-//    Epilogue: reaction + explicit update with the reference's rounding order,
-//    boundary ring pinned to zero, non-finite detection (atomicMin of the step
-//    number), u^{k+1} (and optionally a snapshot copy) stored.
-//  * The path is HBM-bound (0.25 flop/B): no tensor cores; the roofline is
-//    8 bytes per history term.
+//  * fg_step_kernel — the fused time step.  A CTA owns tiles of TP points (one
+//    member each).  Per step k:
+//      A  schedule of step k built in shared memory (segment table → slice index
+//         k-m and coefficient w·ψ_b(m), rounded once exactly like solver.py:190);
+//         every history slice with m >= 2 is streamed with 128-bit loads, 8 in
+//         flight per thread, fp64 FMA into per-tile partial sums.  When tiles are
+//         small the CTA's warps split the entry list S ways and combine in a
+//         fixed order (deterministic).
+//      -- dependency on step k-1 (grid barrier / griddepcontrol.wait) --
+//      C  m = 1 (H[k-1]) and m = 0 (δ^k = stencil(u^k), bit-exact, stored to H[k]),
+//         reaction + explicit update in the reference's rounding order, ring
+//         pinned to zero, non-finite detection, u^{k+1} (+ snapshot) stored.
+//    The same kernel runs one step per launch (fg_step, PDL/graph pipelines) or
+//    every step in one cooperative launch with a split arrive/wait grid barrier
+//    (FG_RUN_PERSISTENT): a CTA arrives after its C phase and only waits after
+//    streaming the next step's A phase, so the barrier latency hides under HBM
+//    traffic and there is no per-step launch or tail.  Same arithmetic in every
+//    mode → bitwise-identical results.
+//  * HBM-bound (0.25 flop/B): no tensor cores; roofline = 8 bytes per term.
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdint.h>
@@ -26,6 +31,7 @@
 #include <string.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/fgb200.h"
 #include "fg_schedule.cuh"
@@ -51,22 +57,53 @@ int cuda_check(cudaError_t e, const char* what) {
 }
 
 constexpr int kThreads = 256;   // 8 warps
+constexpr int kMinBlocks = 4;   // resident CTAs per SM the register budget targets
 constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit load)
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
+constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
 
 // ---------------------------------------------------------------- PTX helpers ---
 
+// History slices: read once per step, never in L1 (.cg keeps the load coherent at
+// L2, which the persistent kernel needs because slices are written mid-launch).
 __device__ __forceinline__ double2 ld_stream(const double* p) {
     double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-                 : "=d"(v.x), "=d"(v.y)
-                 : "l"(p));
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
     return v;
 }
 
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ double2 ld_cg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+
 __device__ __forceinline__ void st_pair(double* p, double a, double b) {
     *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Split grid barrier.  arrive: every thread's writes of this CTA are released
+// (bar.sync + gpu-scope fence by the arriving thread); wait: acquire, then the
+// CTA proceeds.  The counter is monotonic within a launch (reset before it).
+__device__ __forceinline__ void grid_arrive(unsigned long long* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+    }
+}
+
+__device__ __forceinline__ void grid_wait(const unsigned long long* bar, unsigned long long target) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire(bar) < target) __nanosleep(40);
+        __threadfence();
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------- stencil ---
@@ -90,35 +127,38 @@ __device__ __forceinline__ bool interior(const Shape& sh, int32_t q) {
     return i0 > 0 && i0 < sh.n0 - 1 && i1 > 0 && i1 < sh.n1 - 1 && i2 > 0 && i2 < sh.n2 - 1;
 }
 
+// u is read through L2 (.cg): in the persistent kernel the field buffers are
+// rewritten every other step, so an L1 copy could be stale.
 template <int NDIM>
 __device__ __forceinline__ double delta_at(const double* __restrict__ u, const Shape& sh, int32_t q,
                                            double c) {
     if (!interior<NDIM>(sh, q)) return 0.0;
     if (NDIM == 1) {
-        return __dsub_rn(__dadd_rn(__ldg(u + q + 1), __ldg(u + q - 1)), __dmul_rn(2.0, c));
+        return __dsub_rn(__dadd_rn(ld_cg(u + q + 1), ld_cg(u + q - 1)), __dmul_rn(2.0, c));
     } else if (NDIM == 2) {
         const int32_t sx = sh.n1;
-        double r = __dadd_rn(__ldg(u + q + sx), __ldg(u + q - sx));
+        double r = __dadd_rn(ld_cg(u + q + sx), ld_cg(u + q - sx));
         r = __dsub_rn(r, __dmul_rn(4.0, c));
-        r = __dadd_rn(r, __ldg(u + q + 1));
-        return __dadd_rn(r, __ldg(u + q - 1));
+        r = __dadd_rn(r, ld_cg(u + q + 1));
+        return __dadd_rn(r, ld_cg(u + q - 1));
     } else {
         const int32_t sy = sh.n2, sx = sh.n1 * sh.n2;
-        double r = __dadd_rn(__ldg(u + q + sx), __ldg(u + q - sx));
+        double r = __dadd_rn(ld_cg(u + q + sx), ld_cg(u + q - sx));
         r = __dsub_rn(r, __dmul_rn(6.0, c));
-        r = __dadd_rn(r, __ldg(u + q + sy));
-        r = __dadd_rn(r, __ldg(u + q - sy));
-        r = __dadd_rn(r, __ldg(u + q + 1));
-        return __dadd_rn(r, __ldg(u + q - 1));
+        r = __dadd_rn(r, ld_cg(u + q + sy));
+        r = __dadd_rn(r, ld_cg(u + q - sy));
+        r = __dadd_rn(r, ld_cg(u + q + 1));
+        return __dadd_rn(r, ld_cg(u + q - 1));
     }
 }
 
 // ---------------------------------------------------------------- fused step ---
 
 struct StepArgs {
-    const double* u_in;
-    double* u_out;
-    double* snap;          // nullable
+    double* u[2];          // ping-pong fields, u^k in u[k & 1]
+    double* snap;          // single-step mode: explicit snapshot target (nullable)
+    double* pool;          // multi-step mode: snapshot pool
+    const int32_t* snap_slot;  // multi-step mode: pool slot of step `done` or -1 (nullable)
     double* H;
     const double* psi;
     const double* decay;
@@ -126,155 +166,223 @@ struct StepArgs {
     const double* dt;
     const int64_t* horizon;
     int64_t* status;
-    int64_t k;
+    unsigned long long* bar;
+    int64_t k0, k1;        // steps [k0, k1)
     int64_t slice_stride;  // B*ms
     int64_t ms;
     int64_t psi_stride;
     int64_t base;
+    int64_t hz_max;        // max short-memory horizon over members
     double vmax, km;
     Shape sh;
     int32_t n_m;
     int32_t kind;
-    int32_t tiles_per_member;
-    int32_t pdl;
+    int32_t tpm;           // tiles per member
+    int32_t total_tiles;
+    int32_t passes;        // tiles per CTA
+    int32_t pdl_wait;      // single-step: launched as a programmatic dependent
+    int32_t pdl_trigger;   // single-step: let the next step launch early
     int32_t m0_from_history;
 };
 
 template <int NDIM, int REACT, int S>
-__global__ void __launch_bounds__(kThreads, 2) fg_step_kernel(const StepArgs a) {
-    constexpr int kCols = (kThreads / 32) / S;   // warps across the tile
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const StepArgs a) {
+    constexpr int kCols = (kThreads / 32) / S;   // warps across a tile
     constexpr int TP = kCols * 32 * kVec;        // points per tile
+    constexpr int kLanes = kCols * 32;           // split-0 threads (one point pair each)
     __shared__ FgSeg segs[FG_MAX_SEGS];
     __shared__ int64_t seg_first[FG_MAX_SEGS + 1];
     __shared__ int s_nseg;
     __shared__ int32_t s_t[kChunk];
+    __shared__ int32_t s_w[kChunk];
     __shared__ double s_c[kChunk];
-    __shared__ double2 s_part[S > 1 ? (S - 1) * kCols * 32 : 1];
-
-    if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (*(volatile const int64_t*)a.status != FG_NO_BAD_STEP) return;  // diverged earlier
+    __shared__ double2 s_part[S > 1 ? (S - 1) * kLanes : 1];
+    extern __shared__ double2 s_acc[];  // [passes][kLanes] partial sums of the A phase
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int col = warp % kCols, split = warp / kCols;
-    const int64_t b = blockIdx.y;
-    const int32_t q = (int32_t)blockIdx.x * TP + col * 64 + lane * kVec;
-    const bool active = q < a.n_m;
-    const int64_t k = a.k;
-    const double* psi_b = a.psi + b * a.psi_stride;
-    const int64_t moff = b * a.ms + q;
+    const int slot = col * 32 + lane;
+    const int G = gridDim.x;
+    const bool multi = a.k1 - a.k0 > 1;
 
-    // schedule of step k as segments (thread 0), prefix of entry counts
-    if (tid == 0) {
-        const int64_t hz = a.kind == 1 ? a.horizon[b] : 0;
-        int n = fg_segments(a.kind, k, a.base, hz, segs);
-        int64_t acc = 0;
-        for (int i = 0; i < n; ++i) {
-            seg_first[i] = acc;
-            acc += segs[i].count;
-        }
-        seg_first[n] = acc;
-        s_nseg = n;
-    }
-
-    // prologue (split 0): δ^k = stencil(u^k) → H[k], the m = 0 term
-    double u0 = 0.0, u1 = 0.0, acc0 = 0.0, acc1 = 0.0;
-    if (split == 0 && active) {
-        const double* ub = a.u_in + b * a.ms;
-        const double2 uu = *reinterpret_cast<const double2*>(ub + q);
-        u0 = uu.x;
-        u1 = uu.y;
-        double d0, d1;
-        if (a.m0_from_history) {
-            const double2 h = *reinterpret_cast<const double2*>(a.H + k * a.slice_stride + moff);
-            d0 = h.x;
-            d1 = h.y;
-        } else {
-            d0 = delta_at<NDIM>(ub, a.sh, q, u0);
-            d1 = (q + 1 < a.n_m) ? delta_at<NDIM>(ub, a.sh, q + 1, u1) : 0.0;
-            st_pair(a.H + k * a.slice_stride + moff, d0, d1);
-        }
-        const double c0 = psi_b[0];  // w_0 * ψ(0) = 1 * 1
-        acc0 = __dmul_rn(c0, d0);
-        acc1 = __dmul_rn(c0, d1);
-    }
-    __syncthreads();
-
-    const int nseg = s_nseg;
-    const int64_t len = seg_first[nseg];
-    const double* hbase = a.H + moff;
-    // entries j = 1..len-1 (j = 0 is m = 0, done above), staged kChunk at a time
-    for (int64_t c0 = 1; c0 < len; c0 += kChunk) {
-        const int cn = (int)((len - c0) < kChunk ? (len - c0) : kChunk);
-        for (int e = tid; e < cn; e += kThreads) {
-            const int64_t j = c0 + e;
-            int si = 0;
-            while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
-            const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
-            s_t[e] = (int32_t)(k - m);
-            s_c[e] = __dmul_rn((double)segs[si].stride, psi_b[m]);
+    for (int64_t k = a.k0; k < a.k1; ++k) {
+        // ================= A: schedule + old slices (m >= 2) =================
+        for (int i = tid; i < a.passes * kLanes; i += kThreads) s_acc[i] = make_double2(0.0, 0.0);
+        if (tid == 0) {
+            int n = fg_segments(a.kind, k, a.base, a.hz_max, segs);
+            int64_t acc = 0;
+            for (int i = 0; i < n; ++i) {
+                seg_first[i] = acc;
+                acc += segs[i].count;
+            }
+            seg_first[n] = acc;
+            s_nseg = n;
         }
         __syncthreads();
-        if (active) {
-            for (int e0 = split; e0 < cn; e0 += S * kUnroll) {
-                double2 v[kUnroll];
-                double c[kUnroll];
+        const int nseg = s_nseg;
+        const int64_t len = seg_first[nseg];
+        // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
+        // m = 1 whenever the schedule has it.  Both depend on step k-1's output
+        // and are summed in phase C; entries from 2 on read slices t <= k-2.
+        const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
+        const int64_t w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
+        const bool has_m1 = len >= 2 && m1 == 1;
+        const int64_t old = has_m1 ? 2 : 1;
+
+        for (int64_t c0 = old; c0 < len; c0 += kChunk) {
+            const int cn = (int)((len - c0) < kChunk ? (len - c0) : kChunk);
+            for (int e = tid; e < cn; e += kThreads) {
+                const int64_t j = c0 + e;
+                int si = 0;
+                while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
+                const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
+                s_t[e] = (int32_t)(k - m);
+                s_w[e] = (int32_t)segs[si].stride;
+            }
+            int64_t cur_member = -1;
+            for (int p = 0; p < a.passes; ++p) {
+                const int tile = blockIdx.x + p * G;
+                if (tile >= a.total_tiles) break;
+                const int64_t b = tile / a.tpm;
+                if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
+                    __syncthreads();
+                    const double* psi_b = a.psi + b * a.psi_stride;
+                    for (int e = tid; e < cn; e += kThreads)
+                        s_c[e] = __dmul_rn((double)s_w[e], __ldg(psi_b + (k - s_t[e])));
+                    __syncthreads();
+                    cur_member = b;
+                }
+                const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+                const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
+                const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
+                double acc0 = 0.0, acc1 = 0.0;
+                if (q < a.n_m) {
+                    const double* hbase = a.H + b * a.ms + q;
+                    for (int e0 = split; e0 < cnb; e0 += S * kUnroll) {
+                        double2 v[kUnroll];
+                        double c[kUnroll];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    const int e = e0 + u * S;
-                    if (e < cn) {
-                        v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
-                        c[u] = s_c[e];
-                    } else {
-                        v[u] = make_double2(0.0, 0.0);
-                        c[u] = 0.0;
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int e = e0 + u * S;
+                            if (e < cnb) {
+                                v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
+                                c[u] = s_c[e];
+                            } else {
+                                v[u] = make_double2(0.0, 0.0);
+                                c[u] = 0.0;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            acc0 = fma(c[u], v[u].x, acc0);
+                            acc1 = fma(c[u], v[u].y, acc1);
+                        }
                     }
                 }
+                if (S > 1) {
+                    if (split > 0) s_part[(split - 1) * kLanes + slot] = make_double2(acc0, acc1);
+                    __syncthreads();
+                    if (split == 0) {
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    acc0 = fma(c[u], v[u].x, acc0);
-                    acc1 = fma(c[u], v[u].y, acc1);
+                        for (int s = 1; s < S; ++s) {
+                            const double2 pp = s_part[(s - 1) * kLanes + slot];
+                            acc0 = __dadd_rn(acc0, pp.x);
+                            acc1 = __dadd_rn(acc1, pp.y);
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (split == 0) {
+                    double2& r = s_acc[p * kLanes + slot];
+                    r.x = __dadd_rn(r.x, acc0);
+                    r.y = __dadd_rn(r.y, acc1);
                 }
             }
+            __syncthreads();  // s_t / s_w / s_c are refilled by the next chunk
         }
-        __syncthreads();
-    }
 
-    if (S > 1) {
-        if (split > 0) s_part[((split - 1) * kCols + col) * 32 + lane] = make_double2(acc0, acc1);
-        __syncthreads();
+        // ================= dependency on step k-1 =================
+        if (multi) {
+            if (k > a.k0) grid_wait(a.bar, (unsigned long long)(k - a.k0) * (unsigned long long)G);
+        } else {
+            if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+            // step k-1 is complete, so every slice t <= k-1 is final: let step k+1
+            // start its A phase in the slots this grid frees
+            if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;");
+        }
+        // u^j non-finite for some j <= k: stop.  A flag for step k+1 raised during
+        // this step's C phase by another CTA is ignored here, so every CTA leaves
+        // at the same step (no CTA can strand the others at the barrier).
+        if (*(volatile const int64_t*)a.status <= k) return;
+
+        // ================= C: m = 1, m = 0, update =================
+        const double* u_in = a.u[k & 1];
+        double* u_out = a.u[(k + 1) & 1];
+        double* snap = a.snap;
+        if (multi) {
+            const int32_t sl = a.snap_slot ? a.snap_slot[k + 1] : -1;
+            snap = sl >= 0 ? a.pool + (int64_t)sl * a.slice_stride : nullptr;
+        }
         if (split == 0) {
-#pragma unroll
-            for (int s = 1; s < S; ++s) {
-                const double2 p = s_part[((s - 1) * kCols + col) * 32 + lane];
-                acc0 = __dadd_rn(acc0, p.x);
-                acc1 = __dadd_rn(acc1, p.y);
+            for (int p = 0; p < a.passes; ++p) {
+                const int tile = blockIdx.x + p * G;
+                if (tile >= a.total_tiles) break;
+                const int64_t b = tile / a.tpm;
+                const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
+                if (q >= a.n_m) continue;
+                const int64_t moff = b * a.ms + q;
+                const double* ub = u_in + b * a.ms;
+                const double* psi_b = a.psi + b * a.psi_stride;
+                const double2 uu = ld_cg2(ub + q);
+                const double u0 = uu.x, u1 = uu.y;
+                double d0, d1;
+                if (a.m0_from_history) {
+                    const double2 h = ld_cg2(a.H + k * a.slice_stride + moff);
+                    d0 = h.x;
+                    d1 = h.y;
+                } else {
+                    d0 = delta_at<NDIM>(ub, a.sh, q, u0);
+                    d1 = (q + 1 < a.n_m) ? delta_at<NDIM>(ub, a.sh, q + 1, u1) : 0.0;
+                    st_pair(a.H + k * a.slice_stride + moff, d0, d1);
+                }
+                const double2 part = s_acc[p * kLanes + slot];
+                double acc0 = part.x, acc1 = part.y;
+                const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+                if (has_m1 && len_b >= 2) {
+                    const double c1 = __dmul_rn((double)w1, __ldg(psi_b + 1));
+                    const double2 h = ld_cg2(a.H + (k - 1) * a.slice_stride + moff);
+                    acc0 = fma(c1, h.x, acc0);
+                    acc1 = fma(c1, h.y, acc1);
+                }
+                const double c0 = __ldg(psi_b);  // w_0 * ψ(0) = 1 * 1
+                acc0 = fma(c0, d0, acc0);
+                acc1 = fma(c0, d1, acc1);
+
+                // solver.py:215-226 rounding order, ring pinned, non-finite check
+                const double diffuse = a.diffuse[b];
+                double n0, n1;
+                if (REACT == 0) {
+                    const double decay = a.decay[b];
+                    n0 = __dadd_rn(__dmul_rn(u0, decay), __dmul_rn(diffuse, acc0));
+                    n1 = __dadd_rn(__dmul_rn(u1, decay), __dmul_rn(diffuse, acc1));
+                } else {
+                    const double dt = a.dt[b];
+                    const double f0 = __ddiv_rn(__dmul_rn(-a.vmax, u0), __dadd_rn(a.km, u0));
+                    const double f1 = __ddiv_rn(__dmul_rn(-a.vmax, u1), __dadd_rn(a.km, u1));
+                    n0 = __dadd_rn(__dadd_rn(u0, __dmul_rn(dt, f0)), __dmul_rn(diffuse, acc0));
+                    n1 = __dadd_rn(__dadd_rn(u1, __dmul_rn(dt, f1)), __dmul_rn(diffuse, acc1));
+                }
+                if (!interior<NDIM>(a.sh, q)) n0 = 0.0;
+                if (q + 1 >= a.n_m || !interior<NDIM>(a.sh, q + 1)) n1 = 0.0;
+                if (!isfinite(n0) || !isfinite(n1))
+                    atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
+                st_pair(u_out + moff, n0, n1);
+                if (snap) st_pair(snap + moff, n0, n1);
             }
         }
+        if (multi) grid_arrive(a.bar);
     }
-    if (split != 0 || !active) return;
-    if (a.pdl) asm volatile("griddepcontrol.launch_dependents;");
-
-    // epilogue: solver.py:215-226 rounding order, ring pinned, non-finite check
-    const double diffuse = a.diffuse[b];
-    double n0, n1;
-    if (REACT == 0) {
-        const double decay = a.decay[b];
-        n0 = __dadd_rn(__dmul_rn(u0, decay), __dmul_rn(diffuse, acc0));
-        n1 = __dadd_rn(__dmul_rn(u1, decay), __dmul_rn(diffuse, acc1));
-    } else {
-        const double dt = a.dt[b];
-        const double f0 = __ddiv_rn(__dmul_rn(-a.vmax, u0), __dadd_rn(a.km, u0));
-        const double f1 = __ddiv_rn(__dmul_rn(-a.vmax, u1), __dadd_rn(a.km, u1));
-        n0 = __dadd_rn(__dadd_rn(u0, __dmul_rn(dt, f0)), __dmul_rn(diffuse, acc0));
-        n1 = __dadd_rn(__dadd_rn(u1, __dmul_rn(dt, f1)), __dmul_rn(diffuse, acc1));
-    }
-    if (!interior<NDIM>(a.sh, q)) n0 = 0.0;
-    if (q + 1 >= a.n_m || !interior<NDIM>(a.sh, q + 1)) n1 = 0.0;
-    if (!isfinite(n0) || !isfinite(n1))
-        atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
-    st_pair(a.u_out + moff, n0, n1);
-    if (a.snap) st_pair(a.snap + moff, n0, n1);
 }
 
 // ------------------------------------------------------------------ ψ tables ---
@@ -360,7 +468,7 @@ __global__ void fg_stencil_kernel(const double* __restrict__ u, double* __restri
 int validate_plan(const fg_plan* p) {
     if (!p) return fail(FG_ERR_ARG, "plan is NULL");
     if (p->ndim < 1 || p->ndim > 3) return fail(FG_ERR_UNSUPPORTED, "ndim must be 1..3, got %d", p->ndim);
-    if (p->B < 1 || p->B > 65535) return fail(FG_ERR_UNSUPPORTED, "members B must be 1..65535");
+    if (p->B < 1 || p->B > (1 << 24)) return fail(FG_ERR_UNSUPPORTED, "members B out of range");
     if (p->n_m < 3 || p->n_m > (int64_t)1 << 30) return fail(FG_ERR_UNSUPPORTED, "points per member out of range");
     if (p->ms < p->n_m || p->ms % 32) return fail(FG_ERR_ARG, "member stride must be >= n_m and a multiple of 32");
     int64_t prod = 1;
@@ -403,19 +511,22 @@ int sm_count() {
     return g_sm_count;
 }
 
-// Pick the split factor: the smallest S whose CTA count reaches two CTAs per SM.
-int choose_split(const fg_plan* p) {
-    if (p->split) return p->split;
-    const int64_t want = 2LL * sm_count();
-    for (int s = 1; s <= 8; s *= 2) {
-        const int64_t tp = (int64_t)((kThreads / 32) / s) * 32 * kVec;
-        const int64_t ctas = ((p->n_m + tp - 1) / tp) * p->B;
-        if (ctas >= want) return s;
-    }
-    return 8;
+int64_t tile_points(int s) { return (int64_t)((kThreads / 32) / s) * 32 * kVec; }
+
+int64_t tiles_of(const fg_plan* p, int s) {
+    const int64_t tp = tile_points(s);
+    return ((p->n_m + tp - 1) / tp) * p->B;
 }
 
-int64_t tile_points(int s) { return (int64_t)((kThreads / 32) / s) * 32 * kVec; }
+// Smallest split S whose tile count reaches the resident-CTA capacity
+// (148 SMs x kMinBlocks): enough loads in flight in one wave.
+int choose_split(const fg_plan* p) {
+    if (p->split) return p->split;
+    const int64_t want = (int64_t)kMinBlocks * sm_count() * 3 / 4;
+    for (int s = 1; s <= 8; s *= 2)
+        if (tiles_of(p, s) >= want) return s;
+    return 8;
+}
 
 typedef void (*StepKernel)(const StepArgs);
 
@@ -435,11 +546,11 @@ StepKernel pick_kernel(int ndim, int react, int s) {
     return react ? pick_s<3, 1>(s) : pick_s<3, 0>(s);
 }
 
-StepArgs make_args(const fg_plan* p, int64_t k, double* snap, int pdl) {
+StepArgs make_args(const fg_plan* p, int s) {
     StepArgs a;
-    a.u_in = p->u_dev[k & 1];
-    a.u_out = p->u_dev[(k + 1) & 1];
-    a.snap = snap;
+    memset(&a, 0, sizeof a);
+    a.u[0] = p->u_dev[0];
+    a.u[1] = p->u_dev[1];
     a.H = p->H_dev;
     a.psi = p->psi_dev;
     a.decay = p->decay_dev;
@@ -447,40 +558,103 @@ StepArgs make_args(const fg_plan* p, int64_t k, double* snap, int pdl) {
     a.dt = p->dt_dev;
     a.horizon = p->horizon_dev;
     a.status = p->status_dev;
-    a.k = k;
+    a.bar = reinterpret_cast<unsigned long long*>(p->status_dev + 1);
     a.slice_stride = p->B * p->ms;
     a.ms = p->ms;
     a.psi_stride = p->psi_stride;
     a.base = p->base;
+    // short memory: the shared schedule covers the longest member horizon; each
+    // member then uses its own prefix 0..min(H_b, k)
+    a.hz_max = p->horizon_max > 0 ? p->horizon_max : INT64_MAX / 4;
     a.vmax = p->vmax;
     a.km = p->km;
     a.sh = shape_of(p);
     a.n_m = (int32_t)p->n_m;
     a.kind = p->kind;
-    a.pdl = pdl;
+    const int64_t tp = tile_points(s);
+    a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
+    a.total_tiles = (int32_t)(a.tpm * p->B);
     a.m0_from_history = (p->step_flags & FG_STEP_M0_FROM_HISTORY) ? 1 : 0;
     return a;
 }
 
-int launch_step(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, int pdl) {
+size_t acc_smem(int s, int passes) { return (size_t)passes * (size_t)((kThreads / 32) / s) * 32 * sizeof(double2); }
+
+// One step, one launch; grid = one CTA per tile.
+int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, int pdl_wait, int pdl_trigger) {
     const int s = choose_split(p);
-    const int64_t tp = tile_points(s);
-    StepArgs a = make_args(p, k, snap, pdl);
-    a.tiles_per_member = (int32_t)((p->n_m + tp - 1) / tp);
+    StepArgs a = make_args(p, s);
+    a.k0 = k;
+    a.k1 = k + 1;
+    a.snap = snap;
+    a.passes = 1;
+    a.pdl_wait = pdl_wait;
+    a.pdl_trigger = pdl_trigger;
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)a.tiles_per_member, (unsigned)p->B, 1);
+    cfg.gridDim = dim3((unsigned)a.total_tiles, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = acc_smem(s, 1);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    if (pdl) {
+    if (pdl_wait) {
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step launch");
+}
+
+// Persistent geometry: G co-resident CTAs, `passes` tiles each.  Returns 0 and
+// leaves *G = 0 if the cooperative grid cannot be co-resident.
+int persistent_geometry(const fg_plan* p, int s, int* G, int* passes) {
+    *G = 0;
+    *passes = 0;
+    StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
+    const int64_t tiles = tiles_of(p, s);
+    for (int ps = 1; ps <= kMaxPasses; ++ps) {
+        const int64_t g = (tiles + ps - 1) / ps;
+        int per_sm = 0;
+        if (int rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, acc_smem(s, ps)),
+                                "occupancy"))
+            return rc;
+        if (per_sm > 0 && g <= (int64_t)per_sm * sm_count()) {
+            *G = (int)g;
+            *passes = ps;
+            return FG_OK;
+        }
+    }
+    return FG_OK;
+}
+
+int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cudaStream_t st, int G, int passes,
+                      int s) {
+    StepArgs a = make_args(p, s);
+    a.k0 = k0;
+    a.k1 = k1;
+    a.pool = pool;
+    a.snap_slot = pool ? p->snap_slot_dev : nullptr;
+    a.passes = passes;
+    StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
+    const size_t smem = acc_smem(s, passes);
+    if (smem > 48 * 1024) {
+        if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                                "smem attribute"))
+            return rc;
+    }
+    if (int rc = cuda_check(cudaMemsetAsync(p->status_dev + 1, 0, sizeof(int64_t), st), "barrier reset")) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step persistent launch");
 }
 
 }  // namespace
@@ -571,8 +745,8 @@ int fg_stencil(const fg_plan* p, const double* u, double* out, void* stream) {
 
 int fg_step(const fg_plan* p, int64_t k, double* snap, void* stream) {
     if (int rc = validate_plan(p)) return rc;
-    if (k < 0 || k + 1 >= p->h_slices + 1 || k >= p->psi_stride) return fail(FG_ERR_ARG, "fg_step: k out of range");
-    return launch_step(p, k, snap, (cudaStream_t)stream, 0);
+    if (k < 0 || k >= p->h_slices || k >= p->psi_stride) return fail(FG_ERR_ARG, "fg_step: k out of range");
+    return launch_single(p, k, snap, (cudaStream_t)stream, 0, 0);
 }
 
 int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, int64_t n_snap, double* pool,
@@ -582,13 +756,47 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
         return fail(FG_ERR_ARG, "fg_run: step range [%lld, %lld) outside history capacity %lld", (long long)k0,
                     (long long)k1, (long long)p->h_slices);
     if (n_snap > 0 && (!snap_steps || !pool)) return fail(FG_ERR_ARG, "fg_run: snapshots need steps and a pool");
+    if (k1 == k0) return FG_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    const int s = choose_split(p);
+
+    if ((flags & FG_RUN_PERSISTENT) && k1 - k0 > 1) {
+        int G = 0, passes = 0;
+        if (int rc = persistent_geometry(p, s, &G, &passes)) return rc;
+        bool snaps_ok = true;
+        if (n_snap > 0) {
+            if (!p->snap_slot_dev) {
+                snaps_ok = false;
+            } else {
+                std::vector<int32_t> slot((size_t)(p->h_slices + 1), -1);
+                for (int64_t i = 0; i < n_snap; ++i)
+                    if (snap_steps[i] > k0 && snap_steps[i] <= k1) slot[(size_t)snap_steps[i]] = (int32_t)i;
+                if (int rc = cuda_check(cudaMemcpyAsync(p->snap_slot_dev, slot.data(), slot.size() * sizeof(int32_t),
+                                                        cudaMemcpyHostToDevice, st),
+                                        "snapshot map"))
+                    return rc;
+                // the pageable source must stay alive until the copy has read it
+                if (int rc = cuda_check(cudaStreamSynchronize(st), "snapshot map sync")) return rc;
+            }
+        }
+        if (G > 0 && snaps_ok) return launch_persistent(p, k0, k1, n_snap > 0 ? pool : nullptr, st, G, passes, s);
+        // fall through to per-step launches
+    }
+
     const int pdl = (flags & FG_RUN_PDL) ? 1 : 0;
     const bool graph = (flags & FG_RUN_GRAPH) != 0;
     const int64_t slice = p->B * p->ms;
+    // Capture into a private stream (the legacy default stream cannot capture),
+    // then replay the graph on the caller's stream.
+    static thread_local cudaStream_t cap_stream = nullptr;
     cudaStream_t cap = st;
     cudaGraph_t g = nullptr;
     if (graph) {
+        if (!cap_stream) {
+            if (int rc = cuda_check(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "capture stream"))
+                return rc;
+        }
+        cap = cap_stream;
         if (int rc = cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture"))
             return rc;
     }
@@ -601,7 +809,7 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
             snap = pool + si * slice;
             ++si;
         }
-        rc = launch_step(p, k, snap, cap, pdl && k > k0);
+        rc = launch_single(p, k, snap, cap, pdl && k > k0, pdl);
     }
     if (graph) {
         cudaError_t e = cudaStreamEndCapture(cap, &g);
@@ -634,8 +842,7 @@ int fg_status(const fg_plan* p, int64_t* first_bad, void* stream) {
 int fg_step_geometry(const fg_plan* p, int64_t* ctas, int32_t* threads, int32_t* split) {
     if (int rc = validate_plan(p)) return rc;
     const int s = choose_split(p);
-    const int64_t tp = tile_points(s);
-    if (ctas) *ctas = ((p->n_m + tp - 1) / tp) * p->B;
+    if (ctas) *ctas = tiles_of(p, s);
     if (threads) *threads = kThreads;
     if (split) *split = s;
     return FG_OK;

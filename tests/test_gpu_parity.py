@@ -305,9 +305,67 @@ def test_run_field_matches_goldens(fg, golden, name, split):
             assert err <= TOL, f"{name} member {b} step {s}: {err:.3e}"
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 3])
-def test_launch_modes_bitwise_identical(fg, golden, flags):
-    """Plain launches, CUDA graph, PDL and graph+PDL give identical bits."""
-    cfg = _field_config_from_golden(fg, golden, "batch_adaptive")
-    ref = fg.run_field(cfg, flags=0).final
-    assert np.array_equal(fg.run_field(cfg, flags=flags).final, ref)
+@pytest.mark.parametrize("flags", [0, 1, 2, 3, 4, 6])
+@pytest.mark.parametrize("name", ["batch_adaptive", "c2_small", "3d_sat_adaptive"])
+def test_launch_modes_bitwise_identical(fg, golden, flags, name):
+    """Per-step launches, CUDA graph, PDL, graph+PDL and the persistent
+    cooperative kernel give identical bits (same arithmetic in every mode)."""
+    if golden.case(name)["kind"] == "nd":
+        cfg = _field_config_from_golden(fg, golden, name)
+    else:
+        p = golden.problem_params(name)
+        cfg = fg.FieldConfig(initial=p["u0"][0], dx=p["dx"], gamma=float(p["gamma"][0]), dt=float(p["dt"][0]),
+                             n_steps=p["n_steps"], reaction=fg.LinearDecay(p["reaction"][1]),
+                             strategy=fg.AdaptiveMemory(int(p["strategy"][1])), snapshot_every=p["snapshot_every"])
+    ref = fg.run_field(cfg, flags=0)
+    got = fg.run_field(cfg, flags=flags)
+    for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
+        assert s0 == s1 and np.array_equal(a0, a1)
+
+
+def test_persistent_multi_pass_ensemble(fg):
+    """More tiles than resident CTAs: the persistent kernel loops over tiles
+    (passes > 1); bitwise equal to per-step launches, members match the oracle."""
+    from oracle import fg_oracle as fo
+
+    rng = np.random.default_rng(9)
+    B, n, steps = 3000, 64, 120
+    x = np.arange(n) / (n - 1)
+    centres = rng.uniform(0.3, 0.7, size=B)
+    u0 = np.exp(-((x[None, :] - centres[:, None]) ** 2) / (2 * 0.05**2))
+    u0[:, 0] = u0[:, -1] = 0.0
+    gam = rng.uniform(0.3, 0.9, size=B)
+    dts = (0.2 * (1 / (n - 1)) ** 2) ** (1 / gam)
+    cfg = fg.FieldConfig(initial=u0, dx=1 / (n - 1), gamma=gam, dt=dts, n_steps=steps,
+                         strategy=fg.AdaptiveMemory(4), batched=True, snapshot_every=40)
+    pers = fg.run_field(cfg, flags=4)
+    plain = fg.run_field(cfg, flags=0)
+    for (_, a), (_, b) in zip(pers.snapshots, plain.snapshots):
+        assert np.array_equal(a, b)
+    idx = [0, 1, 1499, 2999]
+    ref = fo.run(fo.OracleProblem(u0=u0[idx], gamma=gam[idx], dt=dts[idx], alpha=1.0, dx=1 / (n - 1),
+                                  reaction=("linear", 0.0), strategy=("adaptive", 4), n_steps=steps,
+                                  snapshot_every=40))
+    for (_, got), (_, want) in zip(pers.snapshots, ref["snapshots"]):
+        for i, b in enumerate(idx):
+            assert normwise(got[b], want[i]) <= TOL
+
+
+def test_progress_chunks_bitwise(fg, golden):
+    """progress_every splits the loop into several launches; results unchanged."""
+    cfg = _field_config_from_golden(fg, golden, "3d_sat_full")
+    a = fg.run_field(cfg).final
+    b = fg.run_field(cfg, progress_every=37).final
+    assert np.array_equal(a, b)
+
+
+def test_divergence_all_modes(fg, golden):
+    u0 = np.zeros((8, 8))
+    u0[4, 4] = 10.0
+    cfg = fg.FieldConfig(initial=u0, dx=1.0, gamma=1.0, dt=1.0, n_steps=500)
+    want = golden.meta["divergence"]
+    for flags in (0, 2, 4):
+        with pytest.raises(fg.DivergenceError) as exc:
+            fg.run_field(cfg, flags=flags)
+        assert exc.value.step == want["step"]
+        assert exc.value.peak == pytest.approx(want["peak"], rel=1e-10)
