@@ -242,6 +242,9 @@ class Stepper:
         plan.horizon_max = max(hz) if p.kind == "short" else 0
         self.plan = plan
         self.k = 0
+        self.pool_host = None
+        self.copy_stream = None
+        self.copied: set[int] = set()
 
     # ---------------------------------------------------------------- driving --
     def reset(self, u0_dev) -> None:
@@ -249,24 +252,49 @@ class Stepper:
         self.u[0].copy_(u0_dev)
         self.status.fill_(_lib.FG_NO_BAD_STEP)
         self.k = 0
+        self.copied = set()
 
     def geometry(self) -> tuple[int, int, int]:
         ctas, thr, spl = C.c_int64(0), C.c_int32(0), C.c_int32(0)
         _lib.check(self.L.fg_step_geometry(C.byref(self.plan), C.byref(ctas), C.byref(thr), C.byref(spl)))
         return ctas.value, thr.value, spl.value
 
-    def advance(self, k1: int, *, flags: int | None = None) -> None:
-        """Launch steps self.k .. k1-1 (asynchronous, stream-ordered)."""
+    def advance(self, k1: int, *, flags: int | None = None, stream_snapshots: bool = False) -> None:
+        """Launch steps self.k .. k1-1 (asynchronous, stream-ordered).
+
+        With ``stream_snapshots`` the launch sequence is cut at every snapshot
+        step and each snapshot is copied to pinned host memory on a side stream
+        while the following steps run (the D2H hides under the stepping loop).
+        """
         k0 = self.k
         if k1 <= k0:
             return
         snaps = [s for s in self.snap_steps if s > 0]
         arr = (C.c_int64 * max(1, len(snaps)))(*snaps)
         pool = self.pool.data_ptr() if self.pool is not None else None
-        rc = self.L.fg_run(C.byref(self.plan), k0, k1, arr, len(snaps), pool,
-                           self.flags if flags is None else flags, _lib.stream_handle())
-        _lib.check(rc, "fg_run")
+        fl = self.flags if flags is None else flags
+        st = _lib.stream_handle()
+        cuts = [(i, s) for i, s in enumerate(snaps) if k0 < s <= k1] if stream_snapshots and snaps else []
+        start = k0
+        for i, s in cuts:
+            _lib.check(self.L.fg_run(C.byref(self.plan), start, s, arr, len(snaps), pool, fl, st), "fg_run")
+            self._copy_out(i)
+            start = s
+        if start < k1:
+            _lib.check(self.L.fg_run(C.byref(self.plan), start, k1, arr, len(snaps), pool, fl, st), "fg_run")
         self.k = k1
+
+    def _copy_out(self, i: int) -> None:
+        torch = self.torch
+        if self.pool_host is None:
+            self.pool_host = torch.empty(self.pool.shape, dtype=torch.float64, pin_memory=True)
+            self.copy_stream = torch.cuda.Stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.copy_stream.wait_event(ev)
+        with torch.cuda.stream(self.copy_stream):
+            self.pool_host[i].copy_(self.pool[i], non_blocking=True)
+        self.copied.add(i)
 
     def run(self, progress_every: int = 0) -> float:
         """Run every step; return the loop's wall time (solver.py:248-257 semantics)."""
@@ -278,13 +306,13 @@ class Stepper:
             for stop in list(range(progress_every, n + 1, progress_every)) + [n]:
                 if stop <= self.k:
                     continue
-                self.advance(stop)
+                self.advance(stop, stream_snapshots=True)
                 torch.cuda.synchronize(self.device)
                 if stop % progress_every == 0:
                     self.raise_if_diverged()
                     log.info("step %d/%d", stop, n)
         else:
-            self.advance(n)
+            self.advance(n, stream_snapshots=True)
         torch.cuda.synchronize(self.device)
         elapsed = time.perf_counter() - t0
         self.raise_if_diverged()
@@ -305,17 +333,33 @@ class Stepper:
 
     # -------------------------------------------------------------- results --
     def fetch_snapshots(self) -> list[tuple[int, np.ndarray]]:
-        """Device pool → host (one D2H copy); step 0 is the input field itself."""
+        """Snapshots as host arrays; step 0 is the input field itself.
+
+        Snapshots already streamed to pinned memory during the run are returned
+        as zero-copy views of that buffer; any others come over in one D2H copy.
+        """
+        torch = self.torch
         B, shape = self.p.batch, self.p.shape
         out = [(0, np.array(self.p.u0, dtype=np.float64).reshape((B,) + shape))]
         later = [s for s in self.snap_steps if s > 0]
         self.d2h_bytes = 0
         if later:
-            host = self.pool.to("cpu", non_blocking=False)
-            self.d2h_bytes = host.numel() * 8
-            arr = host.numpy().reshape(len(later), B, self.ms)[:, :, : self.n_m]
+            if self.copy_stream is not None:
+                self.copy_stream.synchronize()
+            missing = [i for i in range(len(later)) if i not in self.copied]
+            if self.pool_host is None:
+                self.pool_host = torch.empty(self.pool.shape, dtype=torch.float64, pin_memory=True)
+            if missing:
+                torch.cuda.synchronize(self.device)
+                if len(missing) == len(later):
+                    self.pool_host.copy_(self.pool)
+                else:
+                    for i in missing:
+                        self.pool_host[i].copy_(self.pool[i])
+            self.d2h_bytes = self.pool_host.numel() * 8
+            arr = self.pool_host.numpy().reshape(len(later), B, self.ms)[:, :, : self.n_m]
             for i, s in enumerate(later):
-                out.append((s, arr[i].reshape((B,) + shape).copy()))
+                out.append((s, arr[i].reshape((B,) + shape)))
         return out
 
     def field(self, k: int | None = None) -> np.ndarray:

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libfgb200.so")
+LIB_PATH = os.environ.get("FGB200_LIB") or os.path.join(HERE, "_lib", "libfgb200.so")
 
 FG_OK = 0
 FG_ERR_ARG = -1

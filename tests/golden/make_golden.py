@@ -301,6 +301,19 @@ def main() -> None:
     dts2 = [0.01 * (b + 1) for b in range(B)]
     record_nd("batch_short", u0s, [0.6] * B, dts2, 1.0e-4, dx, ("linear", 0.0), ShortMemory(0.4), 300, 60)
 
+    # ---- drivers on top of the path: benchmark.py:69-193 ------------------------------
+    from fracgrid.benchmark import gamma_sweep, run_comparison
+
+    cmp_cfg = replace(point, n_steps=300)
+    recs = run_comparison(cmp_cfg, (0.5, 0.9), (10.0, 50.0), (3, 5))
+    meta["comparison"] = [[r.strategy, r.param, r.gamma, r.err_l2_pct, r.err_linf_pct, r.message] for r in recs]
+    sweep_cfg = replace(spread, n_steps=60, snapshot_every=10)
+    meta["sweep_gammas"] = [0.5, 0.75, 1.0]
+    for e in gamma_sweep(sweep_cfg, (0.5, 0.75, 1.0)):
+        arrays[f"sweep_{e.gamma}_profile"] = e.profile
+        arrays[f"sweep_{e.gamma}_steps"] = e.trace_steps
+        arrays[f"sweep_{e.gamma}_values"] = e.trace_values
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)

@@ -1,0 +1,140 @@
+"""BASELINE.json configurations c1-c5 at their full grid sizes on the GPU.
+
+Parity against the C restatement of the reference (oracle/fg_oracle.c, bitwise
+equal to the NumPy restatement and to the reference goldens) on exact prefixes
+and member subsets (both are exact-parity sub-problems), plus
+size-independent properties at the full lengths: power-of-two linearity (bitwise
+for the linear problems), member independence, determinism.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def normwise(got, want):
+    scale = float(np.abs(want).max())
+    return float(np.abs(np.asarray(got) - np.asarray(want)).max()) / scale
+
+
+@pytest.fixture(scope="module")
+def W(cuda_device):
+    from paper_1004_5128_b200 import workloads
+
+    return workloads
+
+
+def oracle_run(cfg, steps=None):
+    from oracle import fg_oracle as fo
+    from oracle import fg_oracle_c as foc
+    from paper_1004_5128_b200._engine import strategy_spec
+
+    p = cfg.to_problem()
+    prob = fo.OracleProblem(u0=p.u0, gamma=p.gamma, dt=p.dt, alpha=p.alpha, dx=p.dx, reaction=p.reaction,
+                            strategy=strategy_spec(cfg.strategy), n_steps=p.n_steps, snapshot_every=p.cadence)
+    return foc.run(prob, max_steps=-1 if steps is None else steps)
+
+
+def compare(res, ref, batched=False):
+    got = dict(res.snapshots)
+    assert [s for s, _ in ref["snapshots"]] == [s for s, _ in res.snapshots]
+    worst = 0.0
+    for s, want in ref["snapshots"]:
+        g = got[s] if batched else got[s][None]
+        for b in range(want.shape[0]):
+            worst = max(worst, normwise(g[b], want[b]))
+    assert worst <= TOL, f"max normwise rel err {worst:.3e}"
+    return worst
+
+
+def test_c1_full_length(W):
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c1()
+    compare(fg.run_field(cfg), oracle_run(cfg))
+
+
+def test_c2_full_length(W):
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c2()
+    compare(fg.run_field(cfg), oracle_run(cfg))
+
+
+@pytest.mark.parametrize("memory", ["full", "short", "adaptive"])
+def test_c3_prefix(W, memory):
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c3(memory, n_steps=160)
+    compare(fg.run_field(cfg), oracle_run(cfg))
+
+
+def test_c3_short_window_engages(W):
+    """Past 500 steps the short window truncates: check at 560 steps (1024²)."""
+    import paper_1004_5128_b200 as fg
+    from dataclasses import replace
+
+    cfg = replace(W.c3("short", n_steps=560), snapshot_every=280)
+    compare(fg.run_field(cfg), oracle_run(cfg))
+
+
+@pytest.mark.parametrize("memory", ["full", "adaptive"])
+def test_c4_prefix(W, memory):
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c4(memory, n_steps=120)
+    compare(fg.run_field(cfg), oracle_run(cfg))
+
+
+def test_c5_member_subset_full_length(W):
+    """All 2048 members for all 10000 steps on the GPU; members 0, 1023, 2047 and
+    the extreme-γ members checked against the oracle run of those members alone."""
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c5()
+    res = fg.run_field(cfg)
+    g = np.asarray(cfg.gamma)
+    idx = sorted({0, 1023, 2047, int(g.argmin()), int(g.argmax())})
+    sub = W.subset_members(cfg, idx)
+    ref = oracle_run(sub)
+    got = dict(res.snapshots)
+    for s, want in ref["snapshots"]:
+        for i, b in enumerate(idx):
+            assert normwise(got[s][b], want[i]) <= TOL, (s, b)
+
+
+def test_c5_member_independence_bitwise(W):
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c5(n_steps=600)
+    full = fg.run_field(cfg).final
+    idx = [5, 700, 2040]
+    alone = fg.run_field(W.subset_members(cfg, idx)).final
+    assert np.array_equal(full[idx], alone)
+
+
+@pytest.mark.parametrize("name", ["c3-adaptive", "c2"])
+def test_power_of_two_linearity_full_length(W, name):
+    """Linear problems: run(2·u0) == 2·run(u0) bit for bit at the full length."""
+    import paper_1004_5128_b200 as fg
+    from dataclasses import replace
+
+    cfg = W.c3("adaptive") if name == "c3-adaptive" else W.c2()
+    a = fg.run_field(cfg).final
+    b = fg.run_field(replace(cfg, initial=2.0 * np.asarray(cfg.initial))).final
+    assert np.array_equal(2.0 * a, b)
+
+
+def test_c4_full_length_determinism_and_sanity(W):
+    """c4 adaptive at full length (4000 steps, 2.1M points): reruns are bitwise
+    identical, the field stays finite and the consumption removes mass."""
+    import paper_1004_5128_b200 as fg
+
+    cfg = W.c4("adaptive")
+    a = fg.run_field(cfg).final
+    b = fg.run_field(cfg).final
+    assert np.array_equal(a, b)
+    assert np.isfinite(a).all() and a.sum() < np.asarray(cfg.initial).sum()

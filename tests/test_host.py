@@ -145,3 +145,20 @@ def test_term_counts_match_oracle():
     assert c5.terms() == fo.count_terms("adaptive", 50, 5) * 3 * 512
     short = W.c3("short", n_steps=600, n=32).to_problem()
     assert short.terms() == fo.count_terms("short", 600, short.param, float(short.dt[0])) * 32 * 32
+
+
+def test_relative_error_matches_reference_formula():
+    from paper_1004_5128_b200.benchmark import BenchmarkRecord, relative_error, source_cell
+
+    ref = np.zeros((5, 5))
+    ref[2, 2], ref[1, 2] = 2.0, 1.0
+    app = ref.copy()
+    app[2, 2] = 1.5
+    l2, linf = relative_error(fg.Grid2D(app, 1.0), fg.Grid2D(ref, 1.0))
+    assert l2 == pytest.approx(0.5 / math.sqrt(5.0) * 100.0)
+    assert linf == pytest.approx(25.0)
+    with pytest.raises(ValueError, match="zero"):
+        relative_error(fg.Grid2D(app, 1.0), fg.Grid2D(np.zeros((5, 5)), 1.0))
+    assert BenchmarkRecord("short", 1.0, 0.5, 0.1, 1.0, 1.0, message="x").failed
+    assert source_cell(make_config(sources=((3, 3, 1.0), (4, 4, -2.0)))) == (4, 4)
+    assert source_cell(make_config(sources=())) == (4, 4)
