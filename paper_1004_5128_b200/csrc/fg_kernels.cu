@@ -245,9 +245,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                 const int tile = blockIdx.x + p * G;
                 if (tile >= a.total_tiles) break;
                 const int64_t b = tile / a.tpm;
-#ifdef FG_INLOOP_PSI
-                const double* psi_t = a.psi + b * a.psi_stride;
-#else
                 if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
                     __syncthreads();
                     const double* psi_b = a.psi + b * a.psi_stride;
@@ -256,7 +253,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                     __syncthreads();
                     cur_member = b;
                 }
-#endif
                 const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
                 const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
                 const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
@@ -271,11 +267,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                             const int e = e0 + u * S;
                             if (e < cnb) {
                                 v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
-#ifdef FG_INLOOP_PSI
-                                c[u] = __dmul_rn((double)s_w[e], __ldg(psi_t + (k - s_t[e])));
-#else
                                 c[u] = s_c[e];
-#endif
                             } else {
                                 v[u] = make_double2(0.0, 0.0);
                                 c[u] = 0.0;

@@ -110,9 +110,10 @@ def test_c5_member_independence_bitwise(W):
     import paper_1004_5128_b200 as fg
 
     cfg = W.c5(n_steps=600)
-    full = fg.run_field(cfg).final
+    # same warp split in both runs (the split fixes the per-point summation order)
+    full = fg.run_field(cfg, split=1).final
     idx = [5, 700, 2040]
-    alone = fg.run_field(W.subset_members(cfg, idx)).final
+    alone = fg.run_field(W.subset_members(cfg, idx), split=1).final
     assert np.array_equal(full[idx], alone)
 
 
