@@ -85,6 +85,9 @@ typedef struct fg_plan {
     int32_t* snap_slot_dev;      /* [h_slices+1] scratch for FG_RUN_PERSISTENT snapshots
                                     (filled by fg_run; NULL if no snapshots)       */
     int64_t horizon_max;         /* host copy of max(horizon_dev) (0 = unknown)    */
+    int32_t tblock;              /* temporal blocking factor: 0 (off), 8 or 16     */
+    int32_t reserved2;
+    double* P_dev;               /* [tblock][B*ms] scratch for blocked partial sums */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of
@@ -151,12 +154,21 @@ int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
 #define FG_RUN_GRAPH 1
 #define FG_RUN_PDL 2
 #define FG_RUN_PERSISTENT 4
+/* Temporal blocking: P_dev already holds the partial sums of the block that
+ * contains k0 (this call continues the previous fg_run of the same plan), so a
+ * block that started before k0 is not recomputed. */
+#define FG_RUN_CONTINUE 16
 int fg_run(const fg_plan* plan, int64_t k0, int64_t k1,
            const int64_t* snap_steps, int64_t n_snap, double* snap_pool_dev,
            int32_t flags, void* stream);
 
 /* Stream-synchronous read of status_dev[0] (first non-finite step). */
 int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);
+
+/* Host accounting for temporal blocking: number of distinct history slices
+ * t < kb0 that the block of steps kb0..kb0+bt-1 reads (the union of their
+ * schedules' old parts), i.e. the slices fg_block_kernel streams once. */
+int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count);
 
 /* Launch geometry fg_step would use: CTAs, threads per CTA, split factor. */
 int fg_step_geometry(const fg_plan* plan, int64_t* ctas, int32_t* threads, int32_t* split);

@@ -59,6 +59,12 @@ def default_flags() -> int:
     return _lib.FG_RUN_PDL
 
 
+def default_tblock() -> int:
+    """Temporal blocking factor (0 = off).  One history pass feeds 16 steps."""
+    env = os.environ.get("FGB200_TBLOCK")
+    return int(env) if env is not None else 16
+
+
 def round_up(n: int, m: int) -> int:
     return (n + m - 1) // m * m
 
@@ -151,6 +157,65 @@ class Problem:
         return total
 
 
+def recent_entries(kind: str, k: int, param: float, horizon: int, mmax: int) -> int:
+    """Entries of schedule(k) with 1 <= m <= mmax (host accounting, schedule.py:70-151)."""
+    if kind in ("full", "short"):
+        top = k if kind == "full" else min(horizon, k)
+        return max(0, min(mmax, top))
+    a = int(param)
+    if k <= a:
+        return max(0, min(mmax, k))
+    n = min(mmax, a)  # dense window 1..a
+    i, a_prev, last = 2, a, None
+    while True:
+        start = a_prev + i
+        if start > k:
+            break
+        a_i, stride = a_prev * a, 2 * i - 1
+        hi = min(a_i, k - i + 1)
+        if hi >= start:
+            cnt = (hi - start) // stride + 1
+            if start <= mmax:
+                n += min(cnt, (mmax - start) // stride + 1)
+            last = (start + (cnt - 1) * stride, i, a_i)
+        a_prev, i = a_i, i + 1
+    tail = a + 1 if last is None else (last[2] + 1 if k > last[2] else last[0] + last[1])
+    if tail <= min(k, mmax):
+        n += min(k, mmax) - tail + 1
+    return n
+
+
+def execution_bytes(p: Problem, tblock: int) -> tuple[int, int]:
+    """(single-pass algorithmic bytes, bytes of the algorithm as executed) for one run.
+
+    Single pass: 8·N per history term + 3·8·N per step (u^k read,
+    u^{k+1} write, δ^k write).  With temporal blocking of factor tb the history
+    is read once per block over the union of the block's old slices, plus the
+    partial sums P (written once, read once per step) and each step's recent
+    entries (1 <= m <= b).
+    """
+    N = p.batch * p.n_m
+    n = int(p.n_steps)
+    single = 8 * p.terms() + 3 * 8 * N * n
+    if not tblock:
+        return single, single
+    L = _lib.load()
+    out = C.c_int64(0)
+    base = int(p.param) if p.kind == "adaptive" else 0
+    members = range(p.batch) if p.kind == "short" else [0]
+    total = 0
+    for b in members:
+        hz = short_horizon(p.param, float(p.dt[b])) if p.kind == "short" else 0
+        for kb0 in range(0, n, tblock):
+            bt = min(tblock, n - kb0)
+            _lib.check(L.fg_block_union(_lib.MEM_KINDS[p.kind], kb0, bt, base, hz, C.byref(out)))
+            total += out.value + bt  # union slices + P write
+            for bb in range(bt):
+                total += 1 + recent_entries(p.kind, kb0 + bb, p.param, hz, bb)  # P read + recent slices
+    scale = p.n_m * 8 * (1 if p.kind == "short" else p.batch)
+    return single, total * scale + 3 * 8 * N * n
+
+
 def check_history_budget(p: Problem) -> None:
     """MemoryBudgetError before any allocation (grid.py:141-146, same formula)."""
     n, B, shape = int(p.n_steps), p.batch, p.shape
@@ -166,7 +231,7 @@ class Stepper:
     """All device state of one run plus the loop driver."""
 
     def __init__(self, problem: Problem, *, device=None, split: int = 0, flags: int | None = None,
-                 snapshots: bool = True):
+                 snapshots: bool = True, tblock: int | None = None):
         import torch
 
         self.torch = torch
@@ -240,11 +305,19 @@ class Stepper:
         plan.status_dev = self.status.data_ptr()
         plan.snap_slot_dev = self.snap_slot.data_ptr() if self.snap_slot is not None else None
         plan.horizon_max = max(hz) if p.kind == "short" else 0
+        tb = default_tblock() if tblock is None else int(tblock)
+        self.P = None
+        if tb and n > tb and not (self.flags & _lib.FG_RUN_PERSISTENT):
+            self.P = torch.empty((tb, slice_elems), **f64)
+            plan.tblock = tb
+            plan.P_dev = self.P.data_ptr()
+        self.tblock = int(plan.tblock)
         self.plan = plan
         self.k = 0
         self.pool_host = None
         self.copy_stream = None
         self.copied: set[int] = set()
+        self._p_block: int | None = None  # block whose partial sums P holds
 
     # ---------------------------------------------------------------- driving --
     def reset(self, u0_dev) -> None:
@@ -253,6 +326,7 @@ class Stepper:
         self.status.fill_(_lib.FG_NO_BAD_STEP)
         self.k = 0
         self.copied = set()
+        self._p_block = None
 
     def geometry(self) -> tuple[int, int, int]:
         ctas, thr, spl = C.c_int64(0), C.c_int32(0), C.c_int32(0)
@@ -276,13 +350,23 @@ class Stepper:
         st = _lib.stream_handle()
         cuts = [(i, s) for i, s in enumerate(snaps) if k0 < s <= k1] if stream_snapshots and snaps else []
         start = k0
-        for i, s in cuts:
-            _lib.check(self.L.fg_run(C.byref(self.plan), start, s, arr, len(snaps), pool, fl, st), "fg_run")
-            self._copy_out(i)
+        for i, s in cuts + [(None, k1)]:
+            if start >= s:
+                continue
+            _lib.check(self.L.fg_run(C.byref(self.plan), start, s, arr, len(snaps), pool,
+                                     fl | self._continue_flag(start), st), "fg_run")
+            if self.tblock:
+                self._p_block = (s - 1) - (s - 1) % self.tblock
+            if i is not None:
+                self._copy_out(i)
             start = s
-        if start < k1:
-            _lib.check(self.L.fg_run(C.byref(self.plan), start, k1, arr, len(snaps), pool, fl, st), "fg_run")
         self.k = k1
+
+    def _continue_flag(self, start: int) -> int:
+        """FG_RUN_CONTINUE when P already holds the partial sums of start's block."""
+        if self.tblock and self._p_block is not None and start - start % self.tblock == self._p_block:
+            return _lib.FG_RUN_CONTINUE
+        return 0
 
     def _copy_out(self, i: int) -> None:
         torch = self.torch

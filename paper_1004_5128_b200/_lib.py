@@ -20,6 +20,7 @@ FG_NO_BAD_STEP = (1 << 63) - 1
 FG_RUN_GRAPH = 1
 FG_RUN_PDL = 2
 FG_RUN_PERSISTENT = 4
+FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
@@ -29,7 +30,7 @@ REACTIONS = {"linear": 0, "saturating": 1}
 EXPORTS = (
     "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
     "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_status",
-    "fg_step_geometry",
+    "fg_step_geometry", "fg_block_union",
 )
 
 
@@ -66,6 +67,9 @@ class FgPlan(C.Structure):
         ("reserved", C.c_int32),
         ("snap_slot_dev", C.c_void_p),
         ("horizon_max", C.c_int64),
+        ("tblock", C.c_int32),
+        ("reserved2", C.c_int32),
+        ("P_dev", C.c_void_p),
     ]
 
 
@@ -91,6 +95,7 @@ def _declare(L):
         "fg_run": (C.c_int, [plan, i64, i64, _p64, i64, vp, i32, vp]),
         "fg_status": (C.c_int, [plan, _p64, vp]),
         "fg_step_geometry": (C.c_int, [plan, _p64, _p32, _p32]),
+        "fg_block_union": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

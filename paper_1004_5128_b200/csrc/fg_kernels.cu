@@ -183,7 +183,31 @@ struct StepArgs {
     int32_t pdl_wait;      // single-step: launched as a programmatic dependent
     int32_t pdl_trigger;   // single-step: let the next step launch early
     int32_t m0_from_history;
+    int32_t blocked;       // temporal blocking: slices t < kb0 come from P
+    int64_t kb0;           // first step of the current block
+    const double* P;       // [tblock][B*ms] block partial sums (fg_block_kernel)
 };
+
+// Number of schedule entries with offset m <= mmax (entries ascend in m).
+__device__ __forceinline__ int64_t entries_upto(const FgSeg* s, int n, int64_t mmax) {
+    int64_t c = 0;
+    for (int i = 0; i < n; ++i) {
+        if (s[i].m0 > mmax) break;
+        const int64_t in = (mmax - s[i].m0) / s[i].stride + 1;
+        c += in < s[i].count ? in : s[i].count;
+    }
+    return c;
+}
+
+// Weight of offset m in a schedule given as ascending segments (0 if absent).
+__device__ __forceinline__ int32_t seg_weight(const FgSeg* s, int n, int64_t m) {
+    for (int i = 0; i < n; ++i) {
+        const int64_t d = m - s[i].m0;
+        if (d < 0) return 0;
+        if (d < s[i].count * s[i].stride) return (d % s[i].stride == 0) ? (int32_t)s[i].stride : 0;
+    }
+    return 0;
+}
 
 template <int NDIM, int REACT, int S>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const StepArgs a) {
@@ -193,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
     __shared__ FgSeg segs[FG_MAX_SEGS];
     __shared__ int64_t seg_first[FG_MAX_SEGS + 1];
     __shared__ int s_nseg;
+    __shared__ int64_t s_lim;
     __shared__ int32_t s_t[kChunk];
     __shared__ int32_t s_w[kChunk];
     __shared__ double s_c[kChunk];
@@ -218,20 +243,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
             }
             seg_first[n] = acc;
             s_nseg = n;
+            // temporal blocking: entries with m > bb (slices t < kb0) are already
+            // summed into P by fg_block_kernel; only m <= bb remain for this step
+            s_lim = a.blocked ? entries_upto(segs, n, k - a.kb0) : acc;
         }
         __syncthreads();
         const int nseg = s_nseg;
         const int64_t len = seg_first[nseg];
+        const int64_t lim = s_lim;
+        const int64_t bb = k - a.kb0;
         // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
         // m = 1 whenever the schedule has it.  Both depend on step k-1's output
         // and are summed in phase C; entries from 2 on read slices t <= k-2.
         const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
         const int64_t w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
-        const bool has_m1 = len >= 2 && m1 == 1;
-        const int64_t old = has_m1 ? 2 : 1;
+        const bool has_m1 = len >= 2 && m1 == 1 && (!a.blocked || bb >= 1);
+        const int64_t old = (len >= 2 && m1 == 1) ? 2 : 1;
 
-        for (int64_t c0 = old; c0 < len; c0 += kChunk) {
-            const int cn = (int)((len - c0) < kChunk ? (len - c0) : kChunk);
+        for (int64_t c0 = old; c0 < lim; c0 += kChunk) {
+            const int cn = (int)((lim - c0) < kChunk ? (lim - c0) : kChunk);
             for (int e = tid; e < cn; e += kThreads) {
                 const int64_t j = c0 + e;
                 int si = 0;
@@ -253,7 +283,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                     __syncthreads();
                     cur_member = b;
                 }
-                const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+                int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+                if (len_b > lim) len_b = lim;
                 const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
                 const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
                 double acc0 = 0.0, acc1 = 0.0;
@@ -348,6 +379,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                 }
                 const double2 part = s_acc[p * kLanes + slot];
                 double acc0 = part.x, acc1 = part.y;
+                if (a.blocked) {  // slices t < kb0, summed by this block's fg_block_kernel
+                    const double2 pb = ld_cg2(a.P + bb * a.slice_stride + moff);
+                    acc0 = __dadd_rn(acc0, pb.x);
+                    acc1 = __dadd_rn(acc1, pb.y);
+                }
                 const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
                 if (has_m1 && len_b >= 2) {
                     const double c1 = __dmul_rn((double)w1, __ldg(psi_b + 1));
@@ -382,6 +418,143 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
             }
         }
         if (multi) grid_arrive(a.bar);
+    }
+}
+
+// ------------------------------------------------------- temporal blocking ---
+// fg_block_kernel: one pass over the history slices t < kb0 feeds the old part of
+// the next `bt` steps (kb0 .. kb0+bt-1) at once:
+//     P[b][p] = Σ_{t < kb0} c_b(t)·H[t][p],  c_b(t) = w·ψ(kb0+b-t) if
+//               kb0+b-t is in the schedule of step kb0+b (weight w), else 0,
+// so each slice of the union of the bt schedules is read from HBM once instead of
+// once per step that visits it (full/short memory: bt× fewer bytes; adaptive:
+// the thinned intervals' strides < bt share slices).  Slices are staged 256 at a
+// time: each thread tests one slice against the bt schedules (segment form),
+// the used ones are compacted into shared memory with their bt coefficients,
+// then streamed with 8 loads in flight and bt FMAs per element.  The step
+// kernel then adds P[b] and only its recent entries (m <= b).
+
+constexpr int kBlkThreads = 256;
+constexpr int kBlkChunk = 256;   // slices examined per stage (one per thread)
+constexpr int kBlkUnroll = 8;
+constexpr int kBlkSegs = 32;     // segments kept per step (host checks the bound)
+
+struct BlockArgs {
+    const double* H;
+    double* P;
+    const double* psi;
+    const int64_t* horizon;
+    int64_t slice_stride, ms, psi_stride, base;
+    int64_t kb0;
+    int32_t bt;
+    int32_t n_m, kind, tpm, total_tiles;
+};
+
+__device__ __forceinline__ double ld_stream1(const double* p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+template <int BT, int S>
+__global__ void __launch_bounds__(kBlkThreads, 3) fg_block_kernel(const BlockArgs a) {
+    constexpr int kCols = (kBlkThreads / 32) / S;
+    constexpr int TP = kCols * 32;  // one point per thread
+    __shared__ FgSeg segs[BT][kBlkSegs];
+    __shared__ int s_nseg[BT];
+    __shared__ int32_t s_t[kBlkChunk];
+    __shared__ double s_c[kBlkChunk * BT];
+    __shared__ int s_cnt[kBlkThreads / 32];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int col = warp % kCols, split = warp / kCols;
+    const int tile = blockIdx.x;
+    const int64_t mem = tile / a.tpm;
+    const int32_t q = (tile % a.tpm) * TP + col * 32 + lane;
+    const bool active = q < a.n_m;
+    const double* psi_b = a.psi + mem * a.psi_stride;
+    if (tid < a.bt) {
+        const int64_t hz = a.kind == 1 ? a.horizon[mem] : 0;
+        s_nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs[tid], kBlkSegs);
+    }
+    __syncthreads();
+
+    double acc[BT];
+#pragma unroll
+    for (int bb = 0; bb < BT; ++bb) acc[bb] = 0.0;
+    const double* hbase = a.H + mem * a.ms + q;
+    for (int64_t t0 = 0; t0 < a.kb0; t0 += kBlkChunk) {
+        // ---- stage: which of the 256 slices t0.. does any step of the block use?
+        const int64_t t = t0 + tid;
+        bool used = false;
+        if (t < a.kb0) {
+            for (int bb = 0; bb < a.bt && !used; ++bb)
+                used = seg_weight(segs[bb], s_nseg[bb], a.kb0 + bb - t) != 0;
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, used);
+        if (lane == 0) s_cnt[warp] = __popc(ballot);
+        __syncthreads();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kBlkThreads / 32; ++w) {
+            before += w < warp ? s_cnt[w] : 0;
+            total += s_cnt[w];
+        }
+        if (used) {  // compacted slot: slice index and its BT coefficients
+            const int pos = before + __popc(ballot & ((1u << lane) - 1u));
+            s_t[pos] = (int32_t)t;
+            for (int bb = 0; bb < BT; ++bb) {
+                double c = 0.0;
+                if (bb < a.bt) {
+                    const int64_t m = a.kb0 + bb - t;
+                    const int32_t w = seg_weight(segs[bb], s_nseg[bb], m);
+                    if (w) c = __dmul_rn((double)w, __ldg(psi_b + m));
+                }
+                s_c[pos * BT + bb] = c;
+            }
+        }
+        __syncthreads();
+        // ---- stream the used slices: one 8-byte load, BT FMAs per element
+        if (active) {
+            for (int e0 = split; e0 < total; e0 += S * kBlkUnroll) {
+                double v[kBlkUnroll];
+#pragma unroll
+                for (int u = 0; u < kBlkUnroll; ++u) {
+                    const int e = e0 + u * S;
+                    v[u] = e < total ? ld_stream1(hbase + (int64_t)s_t[e] * a.slice_stride) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kBlkUnroll; ++u) {
+                    const int e = e0 + u * S;
+                    if (e < total) {
+                        const double* cc = s_c + e * BT;
+#pragma unroll
+                        for (int bb = 0; bb < BT; ++bb) acc[bb] = fma(cc[bb], v[u], acc[bb]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (S > 1) {  // fixed-order combine of the split partial sums (s_c reused)
+        if (split > 0) {
+#pragma unroll
+            for (int bb = 0; bb < BT; ++bb) s_c[((split - 1) * TP + col * 32 + lane) * BT + bb] = acc[bb];
+        }
+        __syncthreads();
+        if (split == 0) {
+            for (int s = 1; s < S; ++s) {
+#pragma unroll
+                for (int bb = 0; bb < BT; ++bb)
+                    acc[bb] = __dadd_rn(acc[bb], s_c[((s - 1) * TP + col * 32 + lane) * BT + bb]);
+            }
+        }
+    }
+    if (split == 0 && active) {
+        double* pout = a.P + mem * a.ms + q;
+#pragma unroll
+        for (int bb = 0; bb < BT; ++bb)
+            if (bb < a.bt) pout[bb * a.slice_stride] = acc[bb];
     }
 }
 
@@ -486,6 +659,14 @@ int validate_plan(const fg_plan* p) {
         return fail(FG_ERR_ARG, "plan has a NULL device pointer");
     if (p->split != 0 && p->split != 1 && p->split != 2 && p->split != 4 && p->split != 8)
         return fail(FG_ERR_ARG, "split must be 0, 1, 2, 4 or 8");
+    if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16)
+        return fail(FG_ERR_ARG, "tblock must be 0, 8 or 16");
+    if (p->tblock && !p->P_dev) return fail(FG_ERR_ARG, "temporal blocking needs P_dev");
+    if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
+        FgSeg s[FG_MAX_SEGS];
+        const int n = fg_segments(p->kind, p->h_slices, p->base, p->horizon_max > 0 ? p->horizon_max : 0, s);
+        if (n > kBlkSegs) return fail(FG_ERR_UNSUPPORTED, "schedule has too many segments for temporal blocking");
+    }
     return FG_OK;
 }
 
@@ -580,8 +761,10 @@ StepArgs make_args(const fg_plan* p, int s) {
 
 size_t acc_smem(int s, int passes) { return (size_t)passes * (size_t)((kThreads / 32) / s) * 32 * sizeof(double2); }
 
-// One step, one launch; grid = one CTA per tile.
-int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, int pdl_wait, int pdl_trigger) {
+// One step, one launch; grid = one CTA per tile.  kb0 >= 0: temporal-blocking
+// mode, slices t < kb0 are taken from plan->P_dev (block starting at kb0).
+int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, int pdl_wait, int pdl_trigger,
+                  int64_t kb0 = -1) {
     const int s = choose_split(p);
     StepArgs a = make_args(p, s);
     a.k0 = k;
@@ -590,6 +773,11 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
     a.passes = 1;
     a.pdl_wait = pdl_wait;
     a.pdl_trigger = pdl_trigger;
+    if (kb0 >= 0) {
+        a.blocked = 1;
+        a.kb0 = kb0;
+        a.P = p->P_dev;
+    }
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.total_tiles, 1, 1);
@@ -604,6 +792,58 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
         cfg.numAttrs = 1;
     }
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step launch");
+}
+
+typedef void (*BlockKernel)(const BlockArgs);
+
+template <int BT>
+BlockKernel pick_block_s(int s) {
+    switch (s) {
+        case 1: return fg_block_kernel<BT, 1>;
+        case 2: return fg_block_kernel<BT, 2>;
+        case 4: return fg_block_kernel<BT, 4>;
+        default: return fg_block_kernel<BT, 8>;
+    }
+}
+
+int64_t block_tiles(const fg_plan* p, int s) {
+    const int64_t tp = (int64_t)((kBlkThreads / 32) / s) * 32;
+    return ((p->n_m + tp - 1) / tp) * p->B;
+}
+
+// Partial sums of the block of steps [kb0, kb0+bt) over slices t < kb0.
+int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
+    if (kb0 <= 0) {  // nothing older than the block: P = 0
+        return cuda_check(cudaMemsetAsync(p->P_dev, 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
+                          "P reset");
+    }
+    int s = 8;
+    const int64_t want = 3LL * sm_count() * 3 / 4;
+    for (int c = 1; c <= 8; c *= 2)
+        if (block_tiles(p, c) >= want) {
+            s = c;
+            break;
+        }
+    BlockArgs a;
+    memset(&a, 0, sizeof a);
+    a.H = p->H_dev;
+    a.P = p->P_dev;
+    a.psi = p->psi_dev;
+    a.horizon = p->horizon_dev;
+    a.slice_stride = p->B * p->ms;
+    a.ms = p->ms;
+    a.psi_stride = p->psi_stride;
+    a.base = p->base;
+    a.kb0 = kb0;
+    a.bt = bt;
+    a.n_m = (int32_t)p->n_m;
+    a.kind = p->kind;
+    const int64_t tp = (int64_t)((kBlkThreads / 32) / s) * 32;
+    a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
+    a.total_tiles = (int32_t)(a.tpm * p->B);
+    BlockKernel kern = p->tblock == 16 ? pick_block_s<16>(s) : pick_block_s<8>(s);
+    kern<<<(unsigned)a.total_tiles, kBlkThreads, 0, st>>>(a);
+    return cuda_check(cudaGetLastError(), "fg_block launch");
 }
 
 // Persistent geometry: G co-resident CTAs, `passes` tiles each.  Returns 0 and
@@ -760,7 +1000,7 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
     cudaStream_t st = (cudaStream_t)stream;
     const int s = choose_split(p);
 
-    if ((flags & FG_RUN_PERSISTENT) && k1 - k0 > 1) {
+    if ((flags & FG_RUN_PERSISTENT) && k1 - k0 > 1 && !p->tblock) {
         int G = 0, passes = 0;
         if (int rc = persistent_geometry(p, s, &G, &passes)) return rc;
         bool snaps_ok = true;
@@ -803,13 +1043,29 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
     int64_t si = 0;
     while (si < n_snap && snap_steps[si] <= k0) ++si;
     int rc = FG_OK;
+    const int64_t tb = p->tblock;
+    const int64_t n_total = p->psi_stride - 1 < p->h_slices - 1 ? p->psi_stride - 1 : p->h_slices - 1;
+    bool after_block = false;
     for (int64_t k = k0; k < k1 && rc == FG_OK; ++k) {
         double* snap = nullptr;
         if (si < n_snap && snap_steps[si] == k + 1) {
             snap = pool + si * slice;
             ++si;
         }
-        rc = launch_single(p, k, snap, cap, pdl && k > k0, pdl);
+        int64_t kb0 = -1;
+        if (tb) {
+            kb0 = k - k % tb;
+            // blocks are aligned to multiples of tb, so a run split into several
+            // fg_run calls recomputes the same partial sums (deterministic)
+            if (k == kb0 || (k == k0 && !(flags & FG_RUN_CONTINUE))) {
+                const int64_t left = n_total - kb0;
+                rc = launch_block(p, kb0, (int)(left < tb ? (left > 0 ? left : 1) : tb), cap);
+                if (rc != FG_OK) break;
+                after_block = true;
+            }
+        }
+        rc = launch_single(p, k, snap, cap, pdl && k > k0 && !after_block, pdl, kb0);
+        after_block = false;
     }
     if (graph) {
         cudaError_t e = cudaStreamEndCapture(cap, &g);
@@ -837,6 +1093,26 @@ int fg_status(const fg_plan* p, int64_t* first_bad, void* stream) {
                             "status copy"))
         return rc;
     return cuda_check(cudaStreamSynchronize(st), "status sync");
+}
+
+int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count) {
+    if (kb0 < 0 || bt < 1 || bt > 64 || !count) return fail(FG_ERR_ARG, "fg_block_union: bad arguments");
+    std::vector<char> used((size_t)kb0, 0);
+    FgSeg s[FG_MAX_SEGS];
+    for (int b = 0; b < bt; ++b) {
+        const int64_t k = kb0 + b;
+        const int n = fg_segments(kind, k, base, horizon, s);
+        if (n < 0) return fail(FG_ERR_ARG, "fg_block_union: invalid schedule");
+        for (int i = 0; i < n; ++i)
+            for (int64_t c = 0; c < s[i].count; ++c) {
+                const int64_t t = k - (s[i].m0 + c * s[i].stride);
+                if (t >= 0 && t < kb0) used[(size_t)t] = 1;
+            }
+    }
+    int64_t u = 0;
+    for (char x : used) u += x;
+    *count = u;
+    return FG_OK;
 }
 
 int fg_step_geometry(const fg_plan* p, int64_t* ctas, int32_t* threads, int32_t* split) {

@@ -30,7 +30,9 @@ struct FgSeg {
 #endif
 
 // Returns the number of segments (>=1) or -1 for invalid arguments.
-FG_HD int fg_segments(int kind, int64_t k, int64_t base, int64_t horizon, FgSeg* s) {
+// `cap` bounds the entries written to s (callers size it; FG_MAX_SEGS suffices
+// for every k < 2^62 and base >= 2).
+FG_HD int fg_segments(int kind, int64_t k, int64_t base, int64_t horizon, FgSeg* s, int cap = FG_MAX_SEGS) {
     if (k < 0) return -1;
     if (kind == 0) {  // full
         s[0].m0 = 0; s[0].count = k + 1; s[0].stride = 1;
@@ -53,7 +55,7 @@ FG_HD int fg_segments(int kind, int64_t k, int64_t base, int64_t horizon, FgSeg*
     bool have = false;
     int64_t last_m = 0, last_i = 0, last_ai = 0;
     int64_t a_prev = a;  // a^(i-1)
-    for (int64_t i = 2; n < FG_MAX_SEGS - 1; ++i) {
+    for (int64_t i = 2; n < cap - 1; ++i) {
         const int64_t start = a_prev + i;
         if (start > k) break;
         const int64_t a_i = a_prev * a;

@@ -317,8 +317,8 @@ def test_launch_modes_bitwise_identical(fg, golden, flags, name):
         cfg = fg.FieldConfig(initial=p["u0"][0], dx=p["dx"], gamma=float(p["gamma"][0]), dt=float(p["dt"][0]),
                              n_steps=p["n_steps"], reaction=fg.LinearDecay(p["reaction"][1]),
                              strategy=fg.AdaptiveMemory(int(p["strategy"][1])), snapshot_every=p["snapshot_every"])
-    ref = fg.run_field(cfg, flags=0)
-    got = fg.run_field(cfg, flags=flags)
+    ref = fg.run_field(cfg, flags=0, tblock=0)
+    got = fg.run_field(cfg, flags=flags, tblock=0)
     for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
         assert s0 == s1 and np.array_equal(a0, a1)
 
@@ -339,7 +339,7 @@ def test_persistent_multi_pass_ensemble(fg):
     cfg = fg.FieldConfig(initial=u0, dx=1 / (n - 1), gamma=gam, dt=dts, n_steps=steps,
                          strategy=fg.AdaptiveMemory(4), batched=True, snapshot_every=40)
     pers = fg.run_field(cfg, flags=4)
-    plain = fg.run_field(cfg, flags=0)
+    plain = fg.run_field(cfg, flags=0, tblock=0)
     for (_, a), (_, b) in zip(pers.snapshots, plain.snapshots):
         assert np.array_equal(a, b)
     idx = [0, 1, 1499, 2999]
@@ -369,3 +369,58 @@ def test_divergence_all_modes(fg, golden):
             fg.run_field(cfg, flags=flags)
         assert exc.value.step == want["step"]
         assert exc.value.peak == pytest.approx(want["peak"], rel=1e-10)
+
+
+# ------------------------------------------------------------ temporal blocking --
+
+def _any_field_config(fg, golden, name):
+    if golden.case(name)["kind"] == "nd":
+        return _field_config_from_golden(fg, golden, name)
+    p = golden.problem_params(name)
+    kind, param = p["strategy"]
+    strat = {"full": lambda: fg.FullMemory(), "short": lambda: fg.ShortMemory(param),
+             "adaptive": lambda: fg.AdaptiveMemory(int(param))}[kind]()
+    return fg.FieldConfig(initial=p["u0"][0], dx=p["dx"], gamma=float(p["gamma"][0]), dt=float(p["dt"][0]),
+                          n_steps=p["n_steps"], alpha=p["alpha"], reaction=fg.LinearDecay(p["reaction"][1]),
+                          strategy=strat, snapshot_every=p["snapshot_every"], history_byte_cap=None)
+
+
+BLOCK_CASES = ["small", "point_full", "point_short100", "point_adaptive3", "point_adaptive5", "c2_small",
+               "c2_small_full", "c2_small_short", "spread_g09_adaptive4"] + ND_CASES
+
+
+@pytest.mark.parametrize("tblock", [8, 16])
+@pytest.mark.parametrize("name", BLOCK_CASES)
+def test_temporal_blocking_matches_goldens(fg, golden, name, tblock):
+    """One history pass feeding `tblock` steps reproduces the reference (≤1e-10)."""
+    cfg = _any_field_config(fg, golden, name)
+    res = fg.run_field(cfg, tblock=tblock)
+    steps, snaps = golden.expected(name)
+    assert [s for s, _ in res.snapshots] == steps.tolist()
+    batched = golden.case(name)["kind"] == "nd"
+    for (s, got), want in zip(res.snapshots, snaps):
+        g = got if batched else got[None]
+        for b in range(want.shape[0]):
+            err = normwise(g[b], want[b])
+            assert err <= TOL, f"{name} tblock {tblock} member {b} step {s}: {err:.3e}"
+
+
+@pytest.mark.parametrize("name", ["c2_small", "batch_short", "3d_sat_full"])
+def test_temporal_blocking_modes_bitwise(fg, golden, name):
+    """Blocked runs are identical across launch modes, across runs split into
+    several launches (partial sums continued or recomputed), and reruns."""
+    cfg = _any_field_config(fg, golden, name)
+    ref = fg.run_field(cfg, flags=0, tblock=16)
+    for kw in (dict(flags=1), dict(flags=2), dict(flags=3), dict(progress_every=7), dict(progress_every=16)):
+        got = fg.run_field(cfg, tblock=16, **kw)
+        for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
+            assert s0 == s1 and np.array_equal(a0, a1), kw
+
+
+def test_temporal_blocking_divergence(fg, golden):
+    u0 = np.zeros((8, 8))
+    u0[4, 4] = 10.0
+    cfg = fg.FieldConfig(initial=u0, dx=1.0, gamma=1.0, dt=1.0, n_steps=500)
+    with pytest.raises(fg.DivergenceError) as exc:
+        fg.run_field(cfg, tblock=16)
+    assert exc.value.step == golden.meta["divergence"]["step"]
