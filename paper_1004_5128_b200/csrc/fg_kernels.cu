@@ -199,15 +199,6 @@ __device__ __forceinline__ int64_t entries_upto(const FgSeg* s, int n, int64_t m
     return c;
 }
 
-// Weight of offset m in a schedule given as ascending segments (0 if absent).
-__device__ __forceinline__ int32_t seg_weight(const FgSeg* s, int n, int64_t m) {
-    for (int i = 0; i < n; ++i) {
-        const int64_t d = m - s[i].m0;
-        if (d < 0) return 0;
-        if (d < s[i].count * s[i].stride) return (d % s[i].stride == 0) ? (int32_t)s[i].stride : 0;
-    }
-    return 0;
-}
 
 template <int NDIM, int REACT, int S>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const StepArgs a) {
@@ -489,7 +480,7 @@ __global__ void __launch_bounds__(kBlkThreads, 3) fg_block_kernel(const BlockArg
         bool used = false;
         if (t < a.kb0) {
             for (int bb = 0; bb < a.bt && !used; ++bb)
-                used = seg_weight(segs[bb], s_nseg[bb], a.kb0 + bb - t) != 0;
+                used = fg_seg_weight(segs[bb], s_nseg[bb], a.kb0 + bb - t) != 0;
         }
         const unsigned ballot = __ballot_sync(0xffffffffu, used);
         if (lane == 0) s_cnt[warp] = __popc(ballot);
@@ -507,7 +498,7 @@ __global__ void __launch_bounds__(kBlkThreads, 3) fg_block_kernel(const BlockArg
                 double c = 0.0;
                 if (bb < a.bt) {
                     const int64_t m = a.kb0 + bb - t;
-                    const int32_t w = seg_weight(segs[bb], s_nseg[bb], m);
+                    const int32_t w = fg_seg_weight(segs[bb], s_nseg[bb], m);
                     if (w) c = __dmul_rn((double)w, __ldg(psi_b + m));
                 }
                 s_c[pos * BT + bb] = c;
@@ -552,6 +543,154 @@ __global__ void __launch_bounds__(kBlkThreads, 3) fg_block_kernel(const BlockArg
     }
     if (split == 0 && active) {
         double* pout = a.P + mem * a.ms + q;
+#pragma unroll
+        for (int bb = 0; bb < BT; ++bb)
+            if (bb < a.bt) pout[bb * a.slice_stride] = acc[bb];
+    }
+}
+
+// ---- TMA-pipelined variant -------------------------------------------------------
+// Same sums as fg_block_kernel, but the history rows are moved by the bulk-copy
+// engine (cp.async.bulk → shared memory, mbarrier complete_tx) instead of
+// per-thread loads: one producer warp keeps kStages × kE slice rows in flight per
+// CTA independent of registers, TP consumer threads (one point each) do the BT
+// FMAs per element from shared memory.  Candidate slices are all t in
+// [t_lo, kb0) (the union covers nearly all of them: full/short memory exactly,
+// adaptive whenever the thinned strides are < BT); slices no step uses get zero
+// coefficients, exactly like the reference's zero-weighted terms.  The
+// coefficient table for the next kCH slices is built by the consumers while the
+// producer's copies for those slices are already in flight.
+
+constexpr int kStages = 4;   // ring depth
+constexpr int kE = 8;        // slice rows per stage
+constexpr int kCH = 256;     // slices per coefficient table (multiple of kE)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int BT, int TP>
+size_t tma_block_smem() {
+    return (size_t)kStages * kE * TP * sizeof(double) + (size_t)kCH * BT * sizeof(double) +
+           2 * kStages * sizeof(uint64_t) + (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int);
+}
+
+template <int BT, int TP>
+__global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* rows = reinterpret_cast<double*>(smem);               // [kStages][kE][TP]
+    double* coef = rows + kStages * kE * TP;                     // [kCH][BT]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kCH * BT);  // [kStages]
+    uint64_t* empty = full + kStages;                            // [kStages]
+    FgSeg* segs = reinterpret_cast<FgSeg*>(empty + kStages);     // [BT][kBlkSegs]
+    int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);    // [BT]
+
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int64_t mem = tile / a.tpm;
+    const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
+    const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+    const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+    const int64_t hz = a.kind == 1 ? a.horizon[mem] : 0;
+    // oldest slice any step of the block can reach: short memory stops at kb0 - H
+    const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
+    const int64_t n_sl = a.kb0 - t_lo;
+    const int64_t n_st = (n_sl + kE - 1) / kE;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TP / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < a.bt) nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
+    __syncthreads();
+
+    if (tid >= TP) {  // ---- producer warp: lane 0 drives the bulk-copy ring
+        if (tid == TP) {
+            const double* src0 = a.H + mem * a.ms + q0;
+            for (int64_t g = 0; g < n_st; ++g) {
+                const int s = (int)(g % kStages);
+                if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
+                const int64_t t0 = t_lo + g * kE;
+                const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
+                mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                for (int e = 0; e < nr; ++e)
+                    bulk_g2s(rows + ((size_t)s * kE + e) * TP, src0 + (t0 + e) * a.slice_stride, row_bytes, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---- consumers: one point per thread
+    const int lane = tid & 31;
+    const double* psi_b = a.psi + mem * a.psi_stride;
+    double acc[BT];
+#pragma unroll
+    for (int bb = 0; bb < BT; ++bb) acc[bb] = 0.0;
+    for (int64_t g = 0; g < n_st; ++g) {
+        const int64_t t0 = t_lo + g * kE;
+        if ((g * kE) % kCH == 0) {  // coefficient table for slices t0 .. t0+kCH-1
+            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            for (int c = tid; c < kCH; c += TP) {
+                const int64_t t = t0 + c;
+#pragma unroll
+                for (int bb = 0; bb < BT; ++bb) {
+                    double v = 0.0;
+                    if (bb < a.bt && t < a.kb0) {
+                        const int64_t m = a.kb0 + bb - t;
+                        const int32_t w = fg_seg_weight(segs + bb * kBlkSegs, nseg[bb], m);
+                        if (w) v = __dmul_rn((double)w, __ldg(psi_b + m));
+                    }
+                    coef[c * BT + bb] = v;
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+        }
+        const int s = (int)(g % kStages);
+        mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
+        const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
+        const double* rs = rows + (size_t)s * kE * TP + tid;
+        const double* cs = coef + ((g * kE) % kCH) * BT;
+        for (int e = 0; e < nr; ++e) {
+            const double v = rs[e * TP];
+#pragma unroll
+            for (int bb = 0; bb < BT; ++bb) acc[bb] = fma(cs[e * BT + bb], v, acc[bb]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (q0 + tid < a.n_m) {
+        double* pout = a.P + mem * a.ms + q0 + tid;
 #pragma unroll
         for (int bb = 0; bb < BT; ++bb)
             if (bb < a.bt) pout[bb * a.slice_stride] = acc[bb];
@@ -841,6 +980,27 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     const int64_t tp = (int64_t)((kBlkThreads / 32) / s) * 32;
     a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
     a.total_tiles = (int32_t)(a.tpm * p->B);
+    static const bool use_ldg = getenv("FGB200_BLOCK_LDG") != nullptr;
+    if (!use_ldg) {  // bulk-copy (TMA engine) pipeline
+        const bool wide = ((p->n_m + 255) / 256) * p->B >= sm_count();
+        const int tp = wide ? 256 : 128;
+        a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
+        a.total_tiles = (int32_t)(a.tpm * p->B);
+        BlockKernel kern;
+        size_t smem;
+        if (p->tblock == 16) {
+            kern = wide ? fg_block_tma_kernel<16, 256> : fg_block_tma_kernel<16, 128>;
+            smem = wide ? tma_block_smem<16, 256>() : tma_block_smem<16, 128>();
+        } else {
+            kern = wide ? fg_block_tma_kernel<8, 256> : fg_block_tma_kernel<8, 128>;
+            smem = wide ? tma_block_smem<8, 256>() : tma_block_smem<8, 128>();
+        }
+        if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                                "block smem attribute"))
+            return rc;
+        kern<<<(unsigned)a.total_tiles, tp + 32, smem, st>>>(a);
+        return cuda_check(cudaGetLastError(), "fg_block_tma launch");
+    }
     BlockKernel kern = p->tblock == 16 ? pick_block_s<16>(s) : pick_block_s<8>(s);
     kern<<<(unsigned)a.total_tiles, kBlkThreads, 0, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block launch");

@@ -83,3 +83,16 @@ FG_HD int64_t fg_schedule_length(const FgSeg* s, int n) {
     for (int i = 0; i < n; ++i) len += s[i].count;
     return len;
 }
+
+// Weight of offset m in a schedule given as ascending segments (0 if absent).
+// A later segment may start inside the stride gap after a segment's last sample
+// (the adaptive tail starts at last_m + last_i < last_m + stride), so the range
+// test stops at the last sample, not at m0 + count*stride.
+FG_HD int32_t fg_seg_weight(const FgSeg* s, int n, int64_t m) {
+    for (int i = 0; i < n; ++i) {
+        const int64_t d = m - s[i].m0;
+        if (d < 0) return 0;
+        if (d <= (s[i].count - 1) * s[i].stride) return (d % s[i].stride == 0) ? (int32_t)s[i].stride : 0;
+    }
+    return 0;
+}
