@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kBlkThreads, 3) fg_block_kernel(const BlockArg
 
 constexpr int kStages = 4;   // ring depth
 constexpr int kE = 8;        // slice rows per stage
-constexpr int kCH = 256;     // slices per coefficient table (multiple of kE)
+constexpr int kCH = 128;     // slices per coefficient table (multiple of kE)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -597,18 +597,40 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Padded shared-memory rows: +4 doubles (32 B) per row puts the 4 k-rows a DMMA
+// B-fragment load touches in disjoint bank quarters (conflict-free LDS.64).
+template <int TP>
+__host__ __device__ constexpr int row_pitch() { return TP + 4; }
+template <int BT>
+__host__ __device__ constexpr int coef_pitch() { return BT + 4; }
+
 template <int BT, int TP>
 size_t tma_block_smem() {
-    return (size_t)kStages * kE * TP * sizeof(double) + (size_t)kCH * BT * sizeof(double) +
+    return (size_t)kStages * kE * row_pitch<TP>() * sizeof(double) + (size_t)kCH * coef_pitch<BT>() * sizeof(double) +
            2 * kStages * sizeof(uint64_t) + (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int);
 }
 
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// The block's old-part sums are a small GEMM per tile: P[BT x TP] += C[BT x 8] ·
+// R[8 x TP] per stage (C = coefficients of 8 slices, R = their rows).  Consumers
+// feed it to the fp64 tensor pipe (DMMA m8n8k4: 256 FMAs per warp instruction,
+// fragments loaded straight from shared memory) instead of 16 FMAs + 9 shared
+// loads per element, which made the scalar version shared-memory-issue bound.
 template <int BT, int TP>
 __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+    constexpr int RP = row_pitch<TP>();
+    constexpr int CP = coef_pitch<BT>();
+    constexpr int MT = BT / 8;  // M tiles (steps)
+    constexpr int NT = 4;       // N tiles of 8 points per warp (32 points)
     extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);               // [kStages][kE][TP]
-    double* coef = rows + kStages * kE * TP;                     // [kCH][BT]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kCH * BT);  // [kStages]
+    double* rows = reinterpret_cast<double*>(smem);                // [kStages][kE][RP]
+    double* coef = rows + kStages * kE * RP;                      // [kCH][CP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kCH * CP);  // [kStages]
     uint64_t* empty = full + kStages;                            // [kStages]
     FgSeg* segs = reinterpret_cast<FgSeg*>(empty + kStages);     // [BT][kBlkSegs]
     int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);    // [BT]
@@ -645,33 +667,46 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
                 const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
                 mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes);
                 for (int e = 0; e < nr; ++e)
-                    bulk_g2s(rows + ((size_t)s * kE + e) * TP, src0 + (t0 + e) * a.slice_stride, row_bytes, &full[s]);
+                    bulk_g2s(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes, &full[s]);
             }
         }
         return;
     }
 
-    // ---- consumers: one point per thread
-    const int lane = tid & 31;
+    // ---- consumers: warp w owns points [32w, 32w+32) of the tile
+    const int lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
     const double* psi_b = a.psi + mem * a.psi_stride;
-    double acc[BT];
+    double d[MT][NT][2];
 #pragma unroll
-    for (int bb = 0; bb < BT; ++bb) acc[bb] = 0.0;
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    const int ngroups = TP / BT;  // threads per step column when filling the table
     for (int64_t g = 0; g < n_st; ++g) {
         const int64_t t0 = t_lo + g * kE;
-        if ((g * kE) % kCH == 0) {  // coefficient table for slices t0 .. t0+kCH-1
+        if ((g * kE) % kCH == 0) {
+            // coefficient table for slices t0 .. t0+kCH-1: zero it, then scatter
+            // w·ψ(m) for every schedule entry of step kb0+bb whose slice falls in
+            // range (segment arithmetic, no per-candidate search)
             asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
-            for (int c = tid; c < kCH; c += TP) {
-                const int64_t t = t0 + c;
-#pragma unroll
-                for (int bb = 0; bb < BT; ++bb) {
-                    double v = 0.0;
-                    if (bb < a.bt && t < a.kb0) {
-                        const int64_t m = a.kb0 + bb - t;
-                        const int32_t w = fg_seg_weight(segs + bb * kBlkSegs, nseg[bb], m);
-                        if (w) v = __dmul_rn((double)w, __ldg(psi_b + m));
+            for (int i = tid; i < kCH * CP; i += TP) coef[i] = 0.0;
+            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            const int bb = tid % BT, grp = tid / BT;
+            if (bb < a.bt) {
+                const int64_t k = a.kb0 + bb;
+                const int64_t t_hi = (t0 + kCH - 1 < a.kb0 - 1) ? t0 + kCH - 1 : a.kb0 - 1;
+                const int64_t m_lo = k - t_hi, m_hi = k - t0;  // offsets mapping into this table
+                const FgSeg* sg = segs + bb * kBlkSegs;
+                for (int si = 0; si < nseg[bb]; ++si) {
+                    const int64_t m0 = sg[si].m0, st = sg[si].stride, last = m0 + (sg[si].count - 1) * st;
+                    const int64_t lo = m_lo > m0 ? m_lo : m0, hi = m_hi < last ? m_hi : last;
+                    if (lo > hi) continue;
+                    const int64_t i0 = (lo - m0 + st - 1) / st, i1 = (hi - m0) / st;
+                    for (int64_t i = i0 + grp; i <= i1; i += ngroups) {
+                        const int64_t m = m0 + i * st;
+                        coef[(k - m - t0) * CP + bb] = __dmul_rn((double)st, __ldg(psi_b + m));
                     }
-                    coef[c * BT + bb] = v;
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
@@ -679,21 +714,35 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
         const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
-        const double* rs = rows + (size_t)s * kE * TP + tid;
-        const double* cs = coef + ((g * kE) % kCH) * BT;
-        for (int e = 0; e < nr; ++e) {
-            const double v = rs[e * TP];
+        const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
+        const double* cs = coef + ((g * kE) % kCH) * CP + fr;
 #pragma unroll
-            for (int bb = 0; bb < BT; ++bb) acc[bb] = fma(cs[e * BT + bb], v, acc[bb]);
+        for (int ks = 0; ks < kE / 4; ++ks) {
+            const int e = ks * 4 + fk;
+            double af[MT], bf[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) af[i] = cs[e * CP + 8 * i];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bf[j] = e < nr ? rs[e * RP + 8 * j] : 0.0;  // partial last stage
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (q0 + tid < a.n_m) {
-        double* pout = a.P + mem * a.ms + q0 + tid;
+    // D fragment: row = step fr (+8 per M tile), columns = 2 adjacent points
+    double* pout = a.P + mem * a.ms + q0 + warp * 32 + fk * 2;
 #pragma unroll
-        for (int bb = 0; bb < BT; ++bb)
-            if (bb < a.bt) pout[bb * a.slice_stride] = acc[bb];
+    for (int i = 0; i < MT; ++i) {
+        const int bb = 8 * i + fr;
+        if (bb >= a.bt) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
+            if (q < a.n_m) st_pair(pout + bb * a.slice_stride + 8 * j, d[i][j][0], d[i][j][1]);
+        }
     }
 }
 
