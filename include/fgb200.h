@@ -170,6 +170,11 @@ int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);
  * schedules' old parts), i.e. the slices fg_block_kernel streams once. */
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count);
 
+/* Temporal blocking building block (normally driven by fg_run): write into
+ * plan->P_dev the partial sums of steps kb0..kb0+bt-1 over history slices
+ * t < kb0 (bt <= plan->tblock).  Exposed for testing the block kernel alone. */
+int fg_block_partials(const fg_plan* plan, int64_t kb0, int32_t bt, void* stream);
+
 /* Launch geometry fg_step would use: CTAs, threads per CTA, split factor. */
 int fg_step_geometry(const fg_plan* plan, int64_t* ctas, int32_t* threads, int32_t* split);
 

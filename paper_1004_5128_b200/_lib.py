@@ -30,7 +30,7 @@ REACTIONS = {"linear": 0, "saturating": 1}
 EXPORTS = (
     "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
     "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_status",
-    "fg_step_geometry", "fg_block_union",
+    "fg_step_geometry", "fg_block_union", "fg_block_partials",
 )
 
 
@@ -96,6 +96,7 @@ def _declare(L):
         "fg_status": (C.c_int, [plan, _p64, vp]),
         "fg_step_geometry": (C.c_int, [plan, _p64, _p32, _p32]),
         "fg_block_union": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
+        "fg_block_partials": (C.c_int, [plan, i64, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

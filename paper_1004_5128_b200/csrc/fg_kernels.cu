@@ -1304,6 +1304,14 @@ int fg_status(const fg_plan* p, int64_t* first_bad, void* stream) {
     return cuda_check(cudaStreamSynchronize(st), "status sync");
 }
 
+int fg_block_partials(const fg_plan* p, int64_t kb0, int32_t bt, void* stream) {
+    if (int rc = validate_plan(p)) return rc;
+    if (!p->tblock) return fail(FG_ERR_ARG, "fg_block_partials: plan has no temporal blocking");
+    if (kb0 < 0 || bt < 1 || bt > p->tblock || kb0 + bt > p->psi_stride || kb0 > p->h_slices)
+        return fail(FG_ERR_ARG, "fg_block_partials: block out of range");
+    return launch_block(p, kb0, bt, (cudaStream_t)stream);
+}
+
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count) {
     if (kb0 < 0 || bt < 1 || bt > 64 || !count) return fail(FG_ERR_ARG, "fg_block_union: bad arguments");
     std::vector<char> used((size_t)kb0, 0);
