@@ -579,6 +579,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
+// Release a ring slot only once the warp's tensor-core work on it has consumed
+// its shared-memory operands: the fake `dep` input (a result of the warp's last
+// DMMA) makes the arrive wait for that DMMA, hence for every LDS feeding the
+// warp-wide DMMAs before it.  Without it ptxas scheduled the arrive right after
+// the LDS *issue*, letting the producer's next bulk copy overwrite rows still
+// being read (a rare, TP-dependent race).
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* b, double dep, double* sink) {
+    asm volatile(
+        "st.shared.f64 [%2], %1;\n\t"
+        "mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)),
+        "d"(dep), "r"(smem_u32(sink))
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -607,7 +621,8 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 template <int BT, int TP>
 size_t tma_block_smem() {
     return (size_t)kStages * kE * row_pitch<TP>() * sizeof(double) + (size_t)kCH * coef_pitch<BT>() * sizeof(double) +
-           2 * kStages * sizeof(uint64_t) + (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int);
+           2 * kStages * sizeof(uint64_t) + (TP / 32) * sizeof(double) + (size_t)BT * kBlkSegs * sizeof(FgSeg) +
+           BT * sizeof(int);
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -632,7 +647,8 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     double* coef = rows + kStages * kE * RP;                      // [kCH][CP]
     uint64_t* full = reinterpret_cast<uint64_t*>(coef + kCH * CP);  // [kStages]
     uint64_t* empty = full + kStages;                            // [kStages]
-    FgSeg* segs = reinterpret_cast<FgSeg*>(empty + kStages);     // [BT][kBlkSegs]
+    double* sink = reinterpret_cast<double*>(empty + kStages);   // [TP/32] release dependencies
+    FgSeg* segs = reinterpret_cast<FgSeg*>(sink + TP / 32);      // [BT][kBlkSegs]
     int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);    // [BT]
 
     const int tid = threadIdx.x;
@@ -730,7 +746,15 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
                 for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (lane == 0) {
+            // depend on every tile's last DMMA, i.e. on every operand read from the slot
+            double dep = 0.0;
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dep = __dadd_rn(dep, d[i][j][1]);
+            mbar_arrive_after(&empty[s], dep, sink + warp);
+        }
     }
     // D fragment: row = step fr (+8 per M tile), columns = 2 adjacent points
     double* pout = a.P + mem * a.ms + q0 + warp * 32 + fk * 2;
@@ -1031,7 +1055,8 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     a.total_tiles = (int32_t)(a.tpm * p->B);
     static const bool use_ldg = getenv("FGB200_BLOCK_LDG") != nullptr;
     if (!use_ldg) {  // bulk-copy (TMA engine) pipeline
-        const bool wide = ((p->n_m + 255) / 256) * p->B >= sm_count();
+        static const char* force_tp = getenv("FGB200_BLOCK_TP");
+        const bool wide = force_tp ? atoi(force_tp) == 256 : ((p->n_m + 255) / 256) * p->B >= sm_count();
         const int tp = wide ? 256 : 128;
         a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
         a.total_tiles = (int32_t)(a.tpm * p->B);

@@ -39,7 +39,8 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     tblock = 8 if (kb0, bt) == (517, 8) else 16
     n_steps = kb0 + bt + 1
     u0 = np.zeros(shape)
-    strat = {"full": fg.FullMemory(), "short": fg.ShortMemory(param), "adaptive": fg.AdaptiveMemory(param)}[kind]
+    strat = {"full": lambda: fg.FullMemory(), "short": lambda: fg.ShortMemory(param),
+             "adaptive": lambda: fg.AdaptiveMemory(param)}[kind]()
     cfg = fg.FieldConfig(initial=u0, dx=1.0, gamma=0.63, dt=1.0, n_steps=n_steps, strategy=strat,
                          history_byte_cap=None)
     st = Stepper(cfg.to_problem(), tblock=tblock)
@@ -49,9 +50,11 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
     torch.cuda.synchronize()
     P1 = st.P[:bt].clone()
-    _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
-    torch.cuda.synchronize()
-    assert torch.equal(P1, st.P[:bt]), "block kernel is not deterministic"
+    for rep in range(5):
+        _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
+        torch.cuda.synchronize()
+        bad = (P1 != st.P[:bt]).nonzero()
+        assert bad.numel() == 0, f"rerun {rep} differs at {bad.shape[0]} places, first {bad[:8].tolist()}"
     n = int(np.prod(shape))
     H = st.H[:kb0, :n].cpu().numpy()
     table = st.psi[0].cpu().numpy()
