@@ -733,28 +733,34 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
         const double* cs = coef + ((g * kE) % kCH) * CP + fr;
 #pragma unroll
+        // all fragments of the stage into registers first ...
+        double af[kE / 4][MT], bf[kE / 4][NT];
+        uint32_t x = 0;
+#pragma unroll
         for (int ks = 0; ks < kE / 4; ++ks) {
             const int e = ks * 4 + fk;
-            double af[MT], bf[NT];
 #pragma unroll
-            for (int i = 0; i < MT; ++i) af[i] = cs[e * CP + 8 * i];
+            for (int i = 0; i < MT; ++i) af[ks][i] = cs[e * CP + 8 * i];
 #pragma unroll
-            for (int j = 0; j < NT; ++j) bf[j] = e < nr ? rs[e * RP + 8 * j] : 0.0;  // partial last stage
+            for (int j = 0; j < NT; ++j) {
+                bf[ks][j] = e < nr ? rs[e * RP + 8 * j] : 0.0;  // partial last stage
+                const unsigned long long w = (unsigned long long)__double_as_longlong(bf[ks][j]);
+                x ^= (uint32_t)w ^ (uint32_t)(w >> 32);
+            }
+        }
+        // ... then release the slot: the warp-wide xor of every lane's loaded row
+        // values makes the arrive wait until all of this warp's shared-memory
+        // reads of the slot have returned (ptxas otherwise issues the arrive right
+        // after the loads are *issued*, racing the producer's next bulk copy).
+        // The coefficients are not in the ring and need no such guard.
+        x = __reduce_xor_sync(0xffffffffu, x);
+        if (lane == 0) mbar_arrive_after(&empty[s], (double)x, sink + warp);
+#pragma unroll
+        for (int ks = 0; ks < kE / 4; ++ks)
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
-        }
-        __syncwarp();
-        if (lane == 0) {
-            // depend on every tile's last DMMA, i.e. on every operand read from the slot
-            double dep = 0.0;
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) dep = __dadd_rn(dep, d[i][j][1]);
-            mbar_arrive_after(&empty[s], dep, sink + warp);
-        }
+                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
     }
     // D fragment: row = step fr (+8 per M tile), columns = 2 adjacent points
     double* pout = a.P + mem * a.ms + q0 + warp * 32 + fk * 2;
