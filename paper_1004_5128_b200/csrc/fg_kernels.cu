@@ -413,21 +413,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
 }
 
 // ------------------------------------------------------- temporal blocking ---
-// fg_block_kernel: one pass over the history slices t < kb0 feeds the old part of
-// the next `bt` steps (kb0 .. kb0+bt-1) at once:
+// fg_block_tma_kernel: one pass over the history slices t < kb0 feeds the old
+// part of the next `bt` steps (kb0 .. kb0+bt-1) at once:
 //     P[b][p] = Σ_{t < kb0} c_b(t)·H[t][p],  c_b(t) = w·ψ(kb0+b-t) if
 //               kb0+b-t is in the schedule of step kb0+b (weight w), else 0,
 // so each slice of the union of the bt schedules is read from HBM once instead of
 // once per step that visits it (full/short memory: bt× fewer bytes; adaptive:
-// the thinned intervals' strides < bt share slices).  Slices are staged 256 at a
-// time: each thread tests one slice against the bt schedules (segment form),
-// the used ones are compacted into shared memory with their bt coefficients,
-// then streamed with 8 loads in flight and bt FMAs per element.  The step
-// kernel then adds P[b] and only its recent entries (m <= b).
+// the thinned intervals' strides < bt share slices).  The step kernel then adds
+// P[b] and only its recent entries (m <= b).
 
-constexpr int kBlkThreads = 256;
-constexpr int kBlkChunk = 256;   // slices examined per stage (one per thread)
-constexpr int kBlkUnroll = 8;
 constexpr int kBlkSegs = 32;     // segments kept per step (host checks the bound)
 
 struct BlockArgs {
@@ -441,120 +435,10 @@ struct BlockArgs {
     int32_t n_m, kind, tpm, total_tiles;
 };
 
-__device__ __forceinline__ double ld_stream1(const double* p) {
-    double v;
-    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-
-template <int BT, int S>
-__global__ void __launch_bounds__(kBlkThreads, 3) fg_block_kernel(const BlockArgs a) {
-    constexpr int kCols = (kBlkThreads / 32) / S;
-    constexpr int TP = kCols * 32;  // one point per thread
-    __shared__ FgSeg segs[BT][kBlkSegs];
-    __shared__ int s_nseg[BT];
-    __shared__ int32_t s_t[kBlkChunk];
-    __shared__ double s_c[kBlkChunk * BT];
-    __shared__ int s_cnt[kBlkThreads / 32];
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int col = warp % kCols, split = warp / kCols;
-    const int tile = blockIdx.x;
-    const int64_t mem = tile / a.tpm;
-    const int32_t q = (tile % a.tpm) * TP + col * 32 + lane;
-    const bool active = q < a.n_m;
-    const double* psi_b = a.psi + mem * a.psi_stride;
-    if (tid < a.bt) {
-        const int64_t hz = a.kind == 1 ? a.horizon[mem] : 0;
-        s_nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs[tid], kBlkSegs);
-    }
-    __syncthreads();
-
-    double acc[BT];
-#pragma unroll
-    for (int bb = 0; bb < BT; ++bb) acc[bb] = 0.0;
-    const double* hbase = a.H + mem * a.ms + q;
-    for (int64_t t0 = 0; t0 < a.kb0; t0 += kBlkChunk) {
-        // ---- stage: which of the 256 slices t0.. does any step of the block use?
-        const int64_t t = t0 + tid;
-        bool used = false;
-        if (t < a.kb0) {
-            for (int bb = 0; bb < a.bt && !used; ++bb)
-                used = fg_seg_weight(segs[bb], s_nseg[bb], a.kb0 + bb - t) != 0;
-        }
-        const unsigned ballot = __ballot_sync(0xffffffffu, used);
-        if (lane == 0) s_cnt[warp] = __popc(ballot);
-        __syncthreads();
-        int before = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kBlkThreads / 32; ++w) {
-            before += w < warp ? s_cnt[w] : 0;
-            total += s_cnt[w];
-        }
-        if (used) {  // compacted slot: slice index and its BT coefficients
-            const int pos = before + __popc(ballot & ((1u << lane) - 1u));
-            s_t[pos] = (int32_t)t;
-            for (int bb = 0; bb < BT; ++bb) {
-                double c = 0.0;
-                if (bb < a.bt) {
-                    const int64_t m = a.kb0 + bb - t;
-                    const int32_t w = fg_seg_weight(segs[bb], s_nseg[bb], m);
-                    if (w) c = __dmul_rn((double)w, __ldg(psi_b + m));
-                }
-                s_c[pos * BT + bb] = c;
-            }
-        }
-        __syncthreads();
-        // ---- stream the used slices: one 8-byte load, BT FMAs per element
-        if (active) {
-            for (int e0 = split; e0 < total; e0 += S * kBlkUnroll) {
-                double v[kBlkUnroll];
-#pragma unroll
-                for (int u = 0; u < kBlkUnroll; ++u) {
-                    const int e = e0 + u * S;
-                    v[u] = e < total ? ld_stream1(hbase + (int64_t)s_t[e] * a.slice_stride) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < kBlkUnroll; ++u) {
-                    const int e = e0 + u * S;
-                    if (e < total) {
-                        const double* cc = s_c + e * BT;
-#pragma unroll
-                        for (int bb = 0; bb < BT; ++bb) acc[bb] = fma(cc[bb], v[u], acc[bb]);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (S > 1) {  // fixed-order combine of the split partial sums (s_c reused)
-        if (split > 0) {
-#pragma unroll
-            for (int bb = 0; bb < BT; ++bb) s_c[((split - 1) * TP + col * 32 + lane) * BT + bb] = acc[bb];
-        }
-        __syncthreads();
-        if (split == 0) {
-            for (int s = 1; s < S; ++s) {
-#pragma unroll
-                for (int bb = 0; bb < BT; ++bb)
-                    acc[bb] = __dadd_rn(acc[bb], s_c[((s - 1) * TP + col * 32 + lane) * BT + bb]);
-            }
-        }
-    }
-    if (split == 0 && active) {
-        double* pout = a.P + mem * a.ms + q;
-#pragma unroll
-        for (int bb = 0; bb < BT; ++bb)
-            if (bb < a.bt) pout[bb * a.slice_stride] = acc[bb];
-    }
-}
-
-// ---- TMA-pipelined variant -------------------------------------------------------
-// Same sums as fg_block_kernel, but the history rows are moved by the bulk-copy
-// engine (cp.async.bulk → shared memory, mbarrier complete_tx) instead of
-// per-thread loads: one producer warp keeps kStages × kE slice rows in flight per
-// CTA independent of registers, TP consumer threads (one point each) do the BT
-// FMAs per element from shared memory.  Candidate slices are all t in
+// The history rows are moved by the bulk-copy engine (cp.async.bulk → shared
+// memory, mbarrier complete_tx): one producer warp keeps kStages × kE slice rows
+// in flight per CTA independent of registers; TP/32 consumer warps turn each
+// stage into DMMA m8n8k4 tiles (below).  Candidate slices are all t in
 // [t_lo, kb0) (the union covers nearly all of them: full/short memory exactly,
 // adaptive whenever the thinned strides are < BT); slices no step uses get zero
 // coefficients, exactly like the reference's zero-weighted terms.  The
@@ -1014,19 +898,42 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
 
 typedef void (*BlockKernel)(const BlockArgs);
 
+struct BlockVariant {
+    BlockKernel kern;
+    size_t smem;
+    int tp;
+};
+
 template <int BT>
-BlockKernel pick_block_s(int s) {
-    switch (s) {
-        case 1: return fg_block_kernel<BT, 1>;
-        case 2: return fg_block_kernel<BT, 2>;
-        case 4: return fg_block_kernel<BT, 4>;
-        default: return fg_block_kernel<BT, 8>;
+BlockVariant block_variant(int tp) {
+    switch (tp) {
+        case 128: return {fg_block_tma_kernel<BT, 128>, tma_block_smem<BT, 128>(), 128};
+        case 160: return {fg_block_tma_kernel<BT, 160>, tma_block_smem<BT, 160>(), 160};
+        case 192: return {fg_block_tma_kernel<BT, 192>, tma_block_smem<BT, 192>(), 192};
+        case 224: return {fg_block_tma_kernel<BT, 224>, tma_block_smem<BT, 224>(), 224};
+        default: return {fg_block_tma_kernel<BT, 256>, tma_block_smem<BT, 256>(), 256};
     }
 }
 
-int64_t block_tiles(const fg_plan* p, int s) {
-    const int64_t tp = (int64_t)((kBlkThreads / 32) / s) * 32;
-    return ((p->n_m + tp - 1) / tp) * p->B;
+// Tile width: the block kernel is bound per SM (fp64 tensor pipe + its share of
+// HBM), so pick the TP (32-point warps, 4..8 per CTA) that minimises the work of
+// the busiest SM, ceil(tiles / SMs) * TP; c2 (65536 points) gets 293 tiles of
+// 224 instead of 256 tiles of 256 that leave 40 SMs half idle.
+BlockVariant choose_block_variant(const fg_plan* p) {
+    static const char* force = getenv("FGB200_BLOCK_TP");
+    const int cands[5] = {256, 224, 192, 160, 128};
+    BlockVariant best = {nullptr, 0, 0};
+    int64_t best_cost = INT64_MAX;
+    for (int tp : cands) {
+        if (force && atoi(force) != tp) continue;
+        const int64_t tiles = ((p->n_m + tp - 1) / tp) * p->B;
+        const int64_t cost = ((tiles + sm_count() - 1) / sm_count()) * tp;
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = p->tblock == 16 ? block_variant<16>(tp) : block_variant<8>(tp);
+        }
+    }
+    return best;
 }
 
 // Partial sums of the block of steps [kb0, kb0+bt) over slices t < kb0.
@@ -1035,13 +942,8 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         return cuda_check(cudaMemsetAsync(p->P_dev, 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
                           "P reset");
     }
-    int s = 8;
-    const int64_t want = 3LL * sm_count() * 3 / 4;
-    for (int c = 1; c <= 8; c *= 2)
-        if (block_tiles(p, c) >= want) {
-            s = c;
-            break;
-        }
+    const BlockVariant v = choose_block_variant(p);
+    if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
     BlockArgs a;
     memset(&a, 0, sizeof a);
     a.H = p->H_dev;
@@ -1056,34 +958,13 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     a.bt = bt;
     a.n_m = (int32_t)p->n_m;
     a.kind = p->kind;
-    const int64_t tp = (int64_t)((kBlkThreads / 32) / s) * 32;
-    a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
+    a.tpm = (int32_t)((p->n_m + v.tp - 1) / v.tp);
     a.total_tiles = (int32_t)(a.tpm * p->B);
-    static const bool use_ldg = getenv("FGB200_BLOCK_LDG") != nullptr;
-    if (!use_ldg) {  // bulk-copy (TMA engine) pipeline
-        static const char* force_tp = getenv("FGB200_BLOCK_TP");
-        const bool wide = force_tp ? atoi(force_tp) == 256 : ((p->n_m + 255) / 256) * p->B >= sm_count();
-        const int tp = wide ? 256 : 128;
-        a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
-        a.total_tiles = (int32_t)(a.tpm * p->B);
-        BlockKernel kern;
-        size_t smem;
-        if (p->tblock == 16) {
-            kern = wide ? fg_block_tma_kernel<16, 256> : fg_block_tma_kernel<16, 128>;
-            smem = wide ? tma_block_smem<16, 256>() : tma_block_smem<16, 128>();
-        } else {
-            kern = wide ? fg_block_tma_kernel<8, 256> : fg_block_tma_kernel<8, 128>;
-            smem = wide ? tma_block_smem<8, 256>() : tma_block_smem<8, 128>();
-        }
-        if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                                "block smem attribute"))
-            return rc;
-        kern<<<(unsigned)a.total_tiles, tp + 32, smem, st>>>(a);
-        return cuda_check(cudaGetLastError(), "fg_block_tma launch");
-    }
-    BlockKernel kern = p->tblock == 16 ? pick_block_s<16>(s) : pick_block_s<8>(s);
-    kern<<<(unsigned)a.total_tiles, kBlkThreads, 0, st>>>(a);
-    return cuda_check(cudaGetLastError(), "fg_block launch");
+    if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
+                            "block smem attribute"))
+        return rc;
+    v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
+    return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
 
 // Persistent geometry: G co-resident CTAs, `passes` tiles each.  Returns 0 and
