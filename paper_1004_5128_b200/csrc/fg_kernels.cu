@@ -447,7 +447,7 @@ struct BlockArgs {
 
 constexpr int kStages = 4;   // ring depth
 constexpr int kE = 8;        // slice rows per stage
-constexpr int kCH = 128;     // slices per coefficient table (multiple of kE)
+constexpr int kCH = 64;      // slices per coefficient table (multiple of kE)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -504,9 +504,9 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 
 template <int BT, int TP>
 size_t tma_block_smem() {
-    return (size_t)kStages * kE * row_pitch<TP>() * sizeof(double) + (size_t)kCH * coef_pitch<BT>() * sizeof(double) +
-           2 * kStages * sizeof(uint64_t) + (TP / 32) * sizeof(double) + (size_t)BT * kBlkSegs * sizeof(FgSeg) +
-           BT * sizeof(int);
+    return (size_t)kStages * kE * row_pitch<TP>() * sizeof(double) +
+           2 * (size_t)kCH * coef_pitch<BT>() * sizeof(double) + (2 * kStages + 4) * sizeof(uint64_t) +
+           (TP / 32) * sizeof(double) + (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int);
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -520,22 +520,28 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // feed it to the fp64 tensor pipe (DMMA m8n8k4: 256 FMAs per warp instruction,
 // fragments loaded straight from shared memory) instead of 16 FMAs + 9 shared
 // loads per element, which made the scalar version shared-memory-issue bound.
+// Warp roles: TP/32 consumer warps, one bulk-copy producer warp, one builder warp
+// that fills the double-buffered coefficient table one chunk (kCH slices) ahead.
 template <int BT, int TP>
-__global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+__global__ void __launch_bounds__(TP + 64, 2) fg_block_tma_kernel(const BlockArgs a) {
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
     constexpr int NT = 4;       // N tiles of 8 points per warp (32 points)
+    constexpr int NW = TP / 32; // consumer warps
     extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);                // [kStages][kE][RP]
-    double* coef = rows + kStages * kE * RP;                      // [kCH][CP]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kCH * CP);  // [kStages]
-    uint64_t* empty = full + kStages;                            // [kStages]
-    double* sink = reinterpret_cast<double*>(empty + kStages);   // [TP/32] release dependencies
-    FgSeg* segs = reinterpret_cast<FgSeg*>(sink + TP / 32);      // [BT][kBlkSegs]
-    int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);    // [BT]
+    double* rows = reinterpret_cast<double*>(smem);                    // [kStages][kE][RP]
+    double* coef = rows + kStages * kE * RP;                          // [2][kCH][CP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + 2 * kCH * CP);  // [kStages]
+    uint64_t* empty = full + kStages;                                 // [kStages]
+    uint64_t* tfull = empty + kStages;                                // [2] table built
+    uint64_t* tempty = tfull + 2;                                     // [2] table consumed
+    double* sink = reinterpret_cast<double*>(tempty + 2);             // [NW] release dependencies
+    FgSeg* segs = reinterpret_cast<FgSeg*>(sink + NW);                // [BT][kBlkSegs]
+    int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);         // [BT]
 
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const int64_t mem = tile / a.tpm;
     const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
@@ -546,19 +552,24 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
     const int64_t n_sl = a.kb0 - t_lo;
     const int64_t n_st = (n_sl + kE - 1) / kE;
+    const int64_t n_ch = (n_sl + kCH - 1) / kCH;
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], TP / 32);
+            mbar_init(&empty[s], NW);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], NW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < a.bt) nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
     __syncthreads();
 
-    if (tid >= TP) {  // ---- producer warp: lane 0 drives the bulk-copy ring
-        if (tid == TP) {
+    if (warp == NW) {  // ---- producer: lane 0 drives the bulk-copy ring
+        if (lane == 0) {
             const double* src0 = a.H + mem * a.ms + q0;
             for (int64_t g = 0; g < n_st; ++g) {
                 const int s = (int)(g % kStages);
@@ -572,51 +583,61 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         }
         return;
     }
-
-    // ---- consumers: warp w owns points [32w, 32w+32) of the tile
-    const int lane = tid & 31, warp = tid >> 5;
-    const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
-    const double* psi_b = a.psi + mem * a.psi_stride;
-    double d[MT][NT][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
-    const int ngroups = TP / BT;  // threads per step column when filling the table
-    for (int64_t g = 0; g < n_st; ++g) {
-        const int64_t t0 = t_lo + g * kE;
-        if ((g * kE) % kCH == 0) {
-            // coefficient table for slices t0 .. t0+kCH-1: zero it, then scatter
-            // w·ψ(m) for every schedule entry of step kb0+bb whose slice falls in
-            // range (segment arithmetic, no per-candidate search)
-            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
-            for (int i = tid; i < kCH * CP; i += TP) coef[i] = 0.0;
-            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
-            const int bb = tid % BT, grp = tid / BT;
-            if (bb < a.bt) {
+    if (warp == NW + 1) {  // ---- builder: coefficient table of chunk c into buffer c & 1
+        const double* psi_b = a.psi + mem * a.psi_stride;
+        for (int64_t c = 0; c < n_ch; ++c) {
+            const int buf = (int)(c & 1);
+            if (c >= 2) mbar_wait(&tempty[buf], (uint32_t)(((c / 2) & 1) ^ 1));
+            double* tab = coef + buf * kCH * CP;
+            const int64_t t0 = t_lo + c * kCH;
+            for (int i = lane; i < kCH * CP; i += 32) tab[i] = 0.0;
+            __syncwarp();
+            // scatter w·ψ(m) for every schedule entry of step kb0+bb whose slice
+            // falls into [t0, t0+kCH) (segment arithmetic, no per-slice search)
+            const int64_t t_hi = (t0 + kCH - 1 < a.kb0 - 1) ? t0 + kCH - 1 : a.kb0 - 1;
+            for (int bb = 0; bb < a.bt; ++bb) {
                 const int64_t k = a.kb0 + bb;
-                const int64_t t_hi = (t0 + kCH - 1 < a.kb0 - 1) ? t0 + kCH - 1 : a.kb0 - 1;
-                const int64_t m_lo = k - t_hi, m_hi = k - t0;  // offsets mapping into this table
+                const int64_t m_lo = k - t_hi, m_hi = k - t0;
                 const FgSeg* sg = segs + bb * kBlkSegs;
                 for (int si = 0; si < nseg[bb]; ++si) {
                     const int64_t m0 = sg[si].m0, st = sg[si].stride, last = m0 + (sg[si].count - 1) * st;
                     const int64_t lo = m_lo > m0 ? m_lo : m0, hi = m_hi < last ? m_hi : last;
                     if (lo > hi) continue;
                     const int64_t i0 = (lo - m0 + st - 1) / st, i1 = (hi - m0) / st;
-                    for (int64_t i = i0 + grp; i <= i1; i += ngroups) {
+                    for (int64_t i = i0 + lane; i <= i1; i += 32) {
                         const int64_t m = m0 + i * st;
-                        coef[(k - m - t0) * CP + bb] = __dmul_rn((double)st, __ldg(psi_b + m));
+                        tab[(k - m - t0) * CP + bb] = __dmul_rn((double)st, __ldg(psi_b + m));
                     }
                 }
             }
-            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            __syncwarp();  // orders every lane's table stores before lane 0's release
+            if (lane == 0) mbar_arrive(&tfull[buf]);
+        }
+        return;
+    }
+
+    // ---- consumers: warp w owns points [32w, 32w+32) of the tile
+    const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
+    double d[MT][NT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    for (int64_t g = 0; g < n_st; ++g) {
+        const int64_t t0 = t_lo + g * kE;
+        const int64_t c = (g * kE) / kCH;
+        const int buf = (int)(c & 1);
+        if ((g * kE) % kCH == 0) {
+            // the previous chunk's table is no longer read (its DMMAs have been
+            // issued, so their operands were loaded): hand it back to the builder
+            if (c >= 1 && lane == 0) mbar_arrive(&tempty[buf ^ 1]);
+            mbar_wait(&tfull[buf], (uint32_t)((c / 2) & 1));
         }
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
         const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
         const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
-        const double* cs = coef + ((g * kE) % kCH) * CP + fr;
-#pragma unroll
+        const double* cs = coef + buf * kCH * CP + ((g * kE) % kCH) * CP + fr;
         // all fragments of the stage into registers first ...
         double af[kE / 4][MT], bf[kE / 4][NT];
         uint32_t x = 0;
@@ -636,7 +657,6 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         // values makes the arrive wait until all of this warp's shared-memory
         // reads of the slot have returned (ptxas otherwise issues the arrive right
         // after the loads are *issued*, racing the producer's next bulk copy).
-        // The coefficients are not in the ring and need no such guard.
         x = __reduce_xor_sync(0xffffffffu, x);
         if (lane == 0) mbar_arrive_after(&empty[s], (double)x, sink + warp);
 #pragma unroll
@@ -963,7 +983,7 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
         return rc;
-    v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
+    v.kern<<<(unsigned)a.total_tiles, v.tp + 64, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
 
