@@ -88,6 +88,7 @@ typedef struct fg_plan {
     int32_t tblock;              /* temporal blocking factor: 0 (off), 8 or 16     */
     int32_t reserved2;
     double* P_dev;               /* [tblock][B*ms] scratch for blocked partial sums */
+    double* blkcoef_dev;         /* [h_slices][20] scratch, single-member blocking   */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of

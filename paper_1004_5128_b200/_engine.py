@@ -311,6 +311,9 @@ class Stepper:
             self.P = torch.empty((tb, slice_elems), **f64)
             plan.tblock = tb
             plan.P_dev = self.P.data_ptr()
+            if B == 1:  # per-block coefficient rows shared by all tiles
+                self.blkcoef = torch.empty((n + 1, 20), **f64)
+                plan.blkcoef_dev = self.blkcoef.data_ptr()
         self.tblock = int(plan.tblock)
         self.plan = plan
         self.k = 0

@@ -70,6 +70,7 @@ class FgPlan(C.Structure):
         ("tblock", C.c_int32),
         ("reserved2", C.c_int32),
         ("P_dev", C.c_void_p),
+        ("blkcoef_dev", C.c_void_p),
     ]
 
 

@@ -433,6 +433,7 @@ struct BlockArgs {
     int64_t kb0;
     int32_t bt;
     int32_t n_m, kind, tpm, total_tiles;
+    const double* gcoef;  // single-member blocks: precomputed coefficient rows (or NULL)
 };
 
 // The history rows are moved by the bulk-copy engine (cp.async.bulk → shared
@@ -447,7 +448,7 @@ struct BlockArgs {
 
 constexpr int kStages = 4;   // ring depth
 constexpr int kE = 8;        // slice rows per stage
-constexpr int kCH = 64;      // slices per coefficient table (multiple of kE)
+constexpr int kCH = 128;     // slices per coefficient table (multiple of kE)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -505,8 +506,9 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 template <int BT, int TP>
 size_t tma_block_smem() {
     return (size_t)kStages * kE * row_pitch<TP>() * sizeof(double) +
-           2 * (size_t)kCH * coef_pitch<BT>() * sizeof(double) + (2 * kStages + 4) * sizeof(uint64_t) +
-           (TP / 32) * sizeof(double) + (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int);
+           (size_t)(kStages * kE > kCH ? kStages * kE : kCH) * coef_pitch<BT>() * sizeof(double) +
+           (2 * kStages) * sizeof(uint64_t) + (TP / 32) * sizeof(double) + (size_t)BT * kBlkSegs * sizeof(FgSeg) +
+           BT * sizeof(int);
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -515,30 +517,59 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
+// Coefficient rows of a block, one per candidate slice t (pitch CP doubles):
+// row[t - t_lo][b] = w·ψ(kb0+b-t) if kb0+b-t is in the schedule of step kb0+b.
+// Single-member runs compute them once per block here (all CTAs of the block
+// kernel then bulk-copy their rows next to the history rows).
+template <int BT>
+__global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out) {
+    constexpr int CP = coef_pitch<BT>();
+    __shared__ FgSeg segs[BT][kBlkSegs];
+    __shared__ int nseg[BT];
+    const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
+    const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
+    if (threadIdx.x < a.bt) nseg[threadIdx.x] = fg_segments(a.kind, a.kb0 + threadIdx.x, a.base, hz, segs[threadIdx.x], kBlkSegs);
+    __syncthreads();
+    const int64_t t = t_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.kb0) return;
+    double* row = out + (t - t_lo) * CP;
+#pragma unroll
+    for (int bb = 0; bb < CP; ++bb) {
+        double c = 0.0;
+        if (bb < a.bt) {
+            const int64_t m = a.kb0 + bb - t;
+            const int32_t w = fg_seg_weight(segs[bb], nseg[bb], m);
+            if (w) c = __dmul_rn((double)w, __ldg(a.psi + m));
+        }
+        row[bb] = c;
+    }
+}
+
 // The block's old-part sums are a small GEMM per tile: P[BT x TP] += C[BT x 8] ·
 // R[8 x TP] per stage (C = coefficients of 8 slices, R = their rows).  Consumers
 // feed it to the fp64 tensor pipe (DMMA m8n8k4: 256 FMAs per warp instruction,
 // fragments loaded straight from shared memory) instead of 16 FMAs + 9 shared
 // loads per element, which made the scalar version shared-memory-issue bound.
-// Warp roles: TP/32 consumer warps, one bulk-copy producer warp, one builder warp
-// that fills the double-buffered coefficient table one chunk (kCH slices) ahead.
+// Coefficients: single member → precomputed rows (fg_block_coef_kernel) copied
+// into the ring with each stage; ensembles (per-member ψ) → a kCH-slice table
+// rebuilt by the consumers at chunk boundaries (scatter over segments).
 template <int BT, int TP>
-__global__ void __launch_bounds__(TP + 64, 2) fg_block_tma_kernel(const BlockArgs a) {
+__global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
     constexpr int NT = 4;       // N tiles of 8 points per warp (32 points)
     constexpr int NW = TP / 32; // consumer warps
+    constexpr int CROWS = kStages * kE > kCH ? kStages * kE : kCH;
     extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);                    // [kStages][kE][RP]
-    double* coef = rows + kStages * kE * RP;                          // [2][kCH][CP]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + 2 * kCH * CP);  // [kStages]
-    uint64_t* empty = full + kStages;                                 // [kStages]
-    uint64_t* tfull = empty + kStages;                                // [2] table built
-    uint64_t* tempty = tfull + 2;                                     // [2] table consumed
-    double* sink = reinterpret_cast<double*>(tempty + 2);             // [NW] release dependencies
-    FgSeg* segs = reinterpret_cast<FgSeg*>(sink + NW);                // [BT][kBlkSegs]
-    int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);         // [BT]
+    double* rows = reinterpret_cast<double*>(smem);                  // [kStages][kE][RP]
+    double* coef = rows + kStages * kE * RP;                        // [CROWS][CP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + CROWS * CP);  // [kStages]
+    uint64_t* empty = full + kStages;                               // [kStages]
+    double* sink = reinterpret_cast<double*>(empty + kStages);      // [NW] release dependencies
+    FgSeg* segs = reinterpret_cast<FgSeg*>(sink + NW);              // [BT][kBlkSegs]
+    int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);       // [BT]
+    const bool staged = a.gcoef != nullptr;  // coefficient rows travel with the stage
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -552,20 +583,16 @@ __global__ void __launch_bounds__(TP + 64, 2) fg_block_tma_kernel(const BlockArg
     const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
     const int64_t n_sl = a.kb0 - t_lo;
     const int64_t n_st = (n_sl + kE - 1) / kE;
-    const int64_t n_ch = (n_sl + kCH - 1) / kCH;
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NW);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], NW);
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < a.bt) nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
+    if (!staged && tid < a.bt)
+        nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
     __syncthreads();
 
     if (warp == NW) {  // ---- producer: lane 0 drives the bulk-copy ring
@@ -576,68 +603,57 @@ __global__ void __launch_bounds__(TP + 64, 2) fg_block_tma_kernel(const BlockArg
                 if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
                 const int64_t t0 = t_lo + g * kE;
                 const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
-                mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
+                mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
                 for (int e = 0; e < nr; ++e)
                     bulk_g2s(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes, &full[s]);
+                if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - t_lo) * CP, cbytes, &full[s]);
             }
-        }
-        return;
-    }
-    if (warp == NW + 1) {  // ---- builder: coefficient table of chunk c into buffer c & 1
-        const double* psi_b = a.psi + mem * a.psi_stride;
-        for (int64_t c = 0; c < n_ch; ++c) {
-            const int buf = (int)(c & 1);
-            if (c >= 2) mbar_wait(&tempty[buf], (uint32_t)(((c / 2) & 1) ^ 1));
-            double* tab = coef + buf * kCH * CP;
-            const int64_t t0 = t_lo + c * kCH;
-            for (int i = lane; i < kCH * CP; i += 32) tab[i] = 0.0;
-            __syncwarp();
-            // scatter w·ψ(m) for every schedule entry of step kb0+bb whose slice
-            // falls into [t0, t0+kCH) (segment arithmetic, no per-slice search)
-            const int64_t t_hi = (t0 + kCH - 1 < a.kb0 - 1) ? t0 + kCH - 1 : a.kb0 - 1;
-            for (int bb = 0; bb < a.bt; ++bb) {
-                const int64_t k = a.kb0 + bb;
-                const int64_t m_lo = k - t_hi, m_hi = k - t0;
-                const FgSeg* sg = segs + bb * kBlkSegs;
-                for (int si = 0; si < nseg[bb]; ++si) {
-                    const int64_t m0 = sg[si].m0, st = sg[si].stride, last = m0 + (sg[si].count - 1) * st;
-                    const int64_t lo = m_lo > m0 ? m_lo : m0, hi = m_hi < last ? m_hi : last;
-                    if (lo > hi) continue;
-                    const int64_t i0 = (lo - m0 + st - 1) / st, i1 = (hi - m0) / st;
-                    for (int64_t i = i0 + lane; i <= i1; i += 32) {
-                        const int64_t m = m0 + i * st;
-                        tab[(k - m - t0) * CP + bb] = __dmul_rn((double)st, __ldg(psi_b + m));
-                    }
-                }
-            }
-            __syncwarp();  // orders every lane's table stores before lane 0's release
-            if (lane == 0) mbar_arrive(&tfull[buf]);
         }
         return;
     }
 
     // ---- consumers: warp w owns points [32w, 32w+32) of the tile
     const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
+    const double* psi_b = a.psi + mem * a.psi_stride;
     double d[MT][NT][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    const int ngroups = TP / BT;  // threads per step column when filling the table
     for (int64_t g = 0; g < n_st; ++g) {
         const int64_t t0 = t_lo + g * kE;
-        const int64_t c = (g * kE) / kCH;
-        const int buf = (int)(c & 1);
-        if ((g * kE) % kCH == 0) {
-            // the previous chunk's table is no longer read (its DMMAs have been
-            // issued, so their operands were loaded): hand it back to the builder
-            if (c >= 1 && lane == 0) mbar_arrive(&tempty[buf ^ 1]);
-            mbar_wait(&tfull[buf], (uint32_t)((c / 2) & 1));
+        if (!staged && (g * kE) % kCH == 0) {
+            // ensemble path: coefficient table for slices t0 .. t0+kCH-1 — zero it,
+            // then scatter w·ψ_b(m) over every schedule segment (no per-slice search)
+            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            for (int i = tid; i < kCH * CP; i += TP) coef[i] = 0.0;
+            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            const int bb = tid % BT, grp = tid / BT;
+            if (bb < a.bt) {
+                const int64_t k = a.kb0 + bb;
+                const int64_t t_hi = (t0 + kCH - 1 < a.kb0 - 1) ? t0 + kCH - 1 : a.kb0 - 1;
+                const int64_t m_lo = k - t_hi, m_hi = k - t0;  // offsets mapping into this table
+                const FgSeg* sg = segs + bb * kBlkSegs;
+                for (int si = 0; si < nseg[bb]; ++si) {
+                    const int64_t m0 = sg[si].m0, st = sg[si].stride, last = m0 + (sg[si].count - 1) * st;
+                    const int64_t lo = m_lo > m0 ? m_lo : m0, hi = m_hi < last ? m_hi : last;
+                    if (lo > hi) continue;
+                    const int64_t i0 = (lo - m0 + st - 1) / st, i1 = (hi - m0) / st;
+                    for (int64_t i = i0 + grp; i <= i1; i += ngroups) {
+                        const int64_t m = m0 + i * st;
+                        coef[(k - m - t0) * CP + bb] = __dmul_rn((double)st, __ldg(psi_b + m));
+                    }
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
         }
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
         const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
         const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
-        const double* cs = coef + buf * kCH * CP + ((g * kE) % kCH) * CP + fr;
+        const double* cs = (staged ? coef + (size_t)s * kE * CP : coef + ((g * kE) % kCH) * CP) + fr;
         // all fragments of the stage into registers first ...
         double af[kE / 4][MT], bf[kE / 4][NT];
         uint32_t x = 0;
@@ -645,7 +661,11 @@ __global__ void __launch_bounds__(TP + 64, 2) fg_block_tma_kernel(const BlockArg
         for (int ks = 0; ks < kE / 4; ++ks) {
             const int e = ks * 4 + fk;
 #pragma unroll
-            for (int i = 0; i < MT; ++i) af[ks][i] = cs[e * CP + 8 * i];
+            for (int i = 0; i < MT; ++i) {
+                af[ks][i] = e < nr ? cs[e * CP + 8 * i] : 0.0;
+                const unsigned long long w = (unsigned long long)__double_as_longlong(af[ks][i]);
+                x ^= (uint32_t)w ^ (uint32_t)(w >> 32);
+            }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 bf[ks][j] = e < nr ? rs[e * RP + 8 * j] : 0.0;  // partial last stage
@@ -653,7 +673,7 @@ __global__ void __launch_bounds__(TP + 64, 2) fg_block_tma_kernel(const BlockArg
                 x ^= (uint32_t)w ^ (uint32_t)(w >> 32);
             }
         }
-        // ... then release the slot: the warp-wide xor of every lane's loaded row
+        // ... then release the slot: the warp-wide xor of every lane's loaded
         // values makes the arrive wait until all of this warp's shared-memory
         // reads of the slot have returned (ptxas otherwise issues the arrive right
         // after the loads are *issued*, racing the producer's next bulk copy).
@@ -983,7 +1003,18 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
         return rc;
-    v.kern<<<(unsigned)a.total_tiles, v.tp + 64, v.smem, st>>>(a);
+    if (p->B == 1 && p->blkcoef_dev) {  // coefficient rows computed once for all tiles
+        const int64_t hz_host = p->kind == 1 ? p->horizon_max : 0;  // B == 1: the member's horizon
+        const int64_t t_lo = (p->kind == 1 && kb0 - hz_host > 0) ? kb0 - hz_host : 0;
+        const unsigned nblk = (unsigned)((kb0 - t_lo + 255) / 256);
+        if (p->tblock == 16)
+            fg_block_coef_kernel<16><<<nblk, 256, 0, st>>>(a, p->blkcoef_dev);
+        else
+            fg_block_coef_kernel<8><<<nblk, 256, 0, st>>>(a, p->blkcoef_dev);
+        if (int rc = cuda_check(cudaGetLastError(), "fg_block_coef launch")) return rc;
+        a.gcoef = p->blkcoef_dev;
+    }
+    v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
 
