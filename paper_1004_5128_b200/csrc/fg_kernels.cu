@@ -519,29 +519,32 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 // Coefficient rows of a block, one per candidate slice t (pitch CP doubles):
 // row[t - t_lo][b] = w·ψ(kb0+b-t) if kb0+b-t is in the schedule of step kb0+b.
-// Single-member runs compute them once per block here (all CTAs of the block
-// kernel then bulk-copy their rows next to the history rows).
+// Single-member runs compute them once per block (all CTAs of the block kernel
+// then bulk-copy their rows next to the history rows): the rows are zeroed
+// (cudaMemsetAsync) and CTA b scatters its step's entries with t < kb0 by
+// walking the schedule segments — no per-slice search, no 64-bit divisions.
 template <int BT>
 __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out) {
     constexpr int CP = coef_pitch<BT>();
-    __shared__ FgSeg segs[BT][kBlkSegs];
-    __shared__ int nseg[BT];
+    __shared__ FgSeg segs[FG_MAX_SEGS];
+    __shared__ int nseg;
+    const int bb = blockIdx.x;
     const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
     const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
-    if (threadIdx.x < a.bt) nseg[threadIdx.x] = fg_segments(a.kind, a.kb0 + threadIdx.x, a.base, hz, segs[threadIdx.x], kBlkSegs);
+    const int64_t k = a.kb0 + bb;
+    if (threadIdx.x == 0) nseg = fg_segments(a.kind, k, a.base, hz, segs);
     __syncthreads();
-    const int64_t t = t_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.kb0) return;
-    double* row = out + (t - t_lo) * CP;
-#pragma unroll
-    for (int bb = 0; bb < CP; ++bb) {
-        double c = 0.0;
-        if (bb < a.bt) {
-            const int64_t m = a.kb0 + bb - t;
-            const int32_t w = fg_seg_weight(segs[bb], nseg[bb], m);
-            if (w) c = __dmul_rn((double)w, __ldg(a.psi + m));
+    for (int si = 0; si < nseg; ++si) {
+        // entries m = m0 + i*stride with t = k - m in [t_lo, kb0), i.e. m >= bb+1
+        const int64_t m0 = segs[si].m0, st = segs[si].stride, cnt = segs[si].count;
+        const int64_t m_min = bb + 1, m_max = k - t_lo;
+        if (m_max < m0 || m_min > m0 + (cnt - 1) * st) continue;
+        const int64_t i0 = m_min > m0 ? (m_min - m0 + st - 1) / st : 0;
+        const int64_t i1 = (m_max - m0) / st < cnt - 1 ? (m_max - m0) / st : cnt - 1;
+        for (int64_t i = i0 + threadIdx.x; i <= i1; i += blockDim.x) {
+            const int64_t m = m0 + i * st;
+            out[(k - m - t_lo) * CP + bb] = __dmul_rn((double)st, __ldg(a.psi + m));
         }
-        row[bb] = c;
     }
 }
 
@@ -1006,11 +1009,14 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (p->B == 1 && p->blkcoef_dev) {  // coefficient rows computed once for all tiles
         const int64_t hz_host = p->kind == 1 ? p->horizon_max : 0;  // B == 1: the member's horizon
         const int64_t t_lo = (p->kind == 1 && kb0 - hz_host > 0) ? kb0 - hz_host : 0;
-        const unsigned nblk = (unsigned)((kb0 - t_lo + 255) / 256);
+        const size_t cp = p->tblock == 16 ? coef_pitch<16>() : coef_pitch<8>();
+        if (int rc = cuda_check(cudaMemsetAsync(p->blkcoef_dev, 0, (size_t)(kb0 - t_lo) * cp * sizeof(double), st),
+                                "coefficient rows reset"))
+            return rc;
         if (p->tblock == 16)
-            fg_block_coef_kernel<16><<<nblk, 256, 0, st>>>(a, p->blkcoef_dev);
+            fg_block_coef_kernel<16><<<bt, 256, 0, st>>>(a, p->blkcoef_dev);
         else
-            fg_block_coef_kernel<8><<<nblk, 256, 0, st>>>(a, p->blkcoef_dev);
+            fg_block_coef_kernel<8><<<bt, 256, 0, st>>>(a, p->blkcoef_dev);
         if (int rc = cuda_check(cudaGetLastError(), "fg_block_coef launch")) return rc;
         a.gcoef = p->blkcoef_dev;
     }
