@@ -307,7 +307,7 @@ class Stepper:
         plan.horizon_max = max(hz) if p.kind == "short" else 0
         tb = default_tblock() if tblock is None else int(tblock)
         self.P = None
-        if tb and n > tb and not (self.flags & _lib.FG_RUN_PERSISTENT):
+        if tb and n > tb:
             self.P = torch.empty((tb, slice_elems), **f64)
             plan.tblock = tb
             plan.P_dev = self.P.data_ptr()
