@@ -333,10 +333,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
             // start its A phase in the slots this grid frees
             if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;");
         }
-        // u^j non-finite for some j <= k: stop.  A flag for step k+1 raised during
-        // this step's C phase by another CTA is ignored here, so every CTA leaves
-        // at the same step (no CTA can strand the others at the barrier).
-        if (*(volatile const int64_t*)a.status <= k) return;
+        // u^j non-finite for some j <= k: this step must not run.  The flag is
+        // loaded now but tested only before the stores, so its L2 round trip
+        // overlaps the C-phase loads.  A flag for step k+1 raised during this
+        // step's C phase by another CTA is ignored, so every CTA leaves at the
+        // same step (no CTA can strand the others at the barrier).
+        const bool live = *(volatile const int64_t*)a.status > k;
 
         // ================= C: m = 1, m = 0, update =================
         const double* u_in = a.u[k & 1];
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                 } else {
                     d0 = delta_at<NDIM>(ub, a.sh, q, u0);
                     d1 = (q + 1 < a.n_m) ? delta_at<NDIM>(ub, a.sh, q + 1, u1) : 0.0;
-                    st_pair(a.H + k * a.slice_stride + moff, d0, d1);
+                    if (live) st_pair(a.H + k * a.slice_stride + moff, d0, d1);
                 }
                 const double2 part = s_acc[p * kLanes + slot];
                 double acc0 = part.x, acc1 = part.y;
@@ -402,12 +404,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
                 }
                 if (!interior<NDIM>(a.sh, q)) n0 = 0.0;
                 if (q + 1 >= a.n_m || !interior<NDIM>(a.sh, q + 1)) n1 = 0.0;
+                if (!live) break;
                 if (!isfinite(n0) || !isfinite(n1))
                     atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
                 st_pair(u_out + moff, n0, n1);
                 if (snap) st_pair(snap + moff, n0, n1);
             }
         }
+        if (!live) return;  // uniform: every thread read the same flag
         if (multi) grid_arrive(a.bar);
     }
 }
@@ -446,7 +450,6 @@ struct BlockArgs {
 // coefficient table for the next kCH slices is built by the consumers while the
 // producer's copies for those slices are already in flight.
 
-constexpr int kStages = 4;   // ring depth
 constexpr int kE = 8;        // slice rows per stage
 constexpr int kCH = 128;     // slices per coefficient table (multiple of kE)
 
@@ -503,12 +506,16 @@ __host__ __device__ constexpr int row_pitch() { return TP + 4; }
 template <int BT>
 __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 
-template <int BT, int TP>
+template <bool STAGED>
+__host__ __device__ constexpr int ring_stages() { return STAGED ? 6 : 4; }
+
+template <int BT, int TP, bool STAGED>
 size_t tma_block_smem() {
-    return (size_t)kStages * kE * row_pitch<TP>() * sizeof(double) +
-           (size_t)(kStages * kE > kCH ? kStages * kE : kCH) * coef_pitch<BT>() * sizeof(double) +
-           (2 * kStages) * sizeof(uint64_t) + (TP / 32) * sizeof(double) + (size_t)BT * kBlkSegs * sizeof(FgSeg) +
-           BT * sizeof(int);
+    constexpr int NS = ring_stages<STAGED>();
+    constexpr int CROWS = STAGED ? NS * kE : kCH;
+    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)CROWS * coef_pitch<BT>() * sizeof(double) +
+           (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double) +
+           (STAGED ? 0 : (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int));
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -556,14 +563,15 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
 // Coefficients: single member → precomputed rows (fg_block_coef_kernel) copied
 // into the ring with each stage; ensembles (per-member ψ) → a kCH-slice table
 // rebuilt by the consumers at chunk boundaries (scatter over segments).
-template <int BT, int TP>
+template <int BT, int TP, bool STAGED>
 __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+    constexpr int kStages = ring_stages<STAGED>();
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
     constexpr int NT = 4;       // N tiles of 8 points per warp (32 points)
     constexpr int NW = TP / 32; // consumer warps
-    constexpr int CROWS = kStages * kE > kCH ? kStages * kE : kCH;
+    constexpr int CROWS = STAGED ? kStages * kE : kCH;
     extern __shared__ __align__(128) unsigned char smem[];
     double* rows = reinterpret_cast<double*>(smem);                  // [kStages][kE][RP]
     double* coef = rows + kStages * kE * RP;                        // [CROWS][CP]
@@ -572,7 +580,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     double* sink = reinterpret_cast<double*>(empty + kStages);      // [NW] release dependencies
     FgSeg* segs = reinterpret_cast<FgSeg*>(sink + NW);              // [BT][kBlkSegs]
     int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);       // [BT]
-    const bool staged = a.gcoef != nullptr;  // coefficient rows travel with the stage
+    constexpr bool staged = STAGED;  // coefficient rows travel with the stage (single member)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -951,14 +959,13 @@ struct BlockVariant {
     int tp;
 };
 
-template <int BT>
+template <int BT, bool ST>
 BlockVariant block_variant(int tp) {
     switch (tp) {
-        case 128: return {fg_block_tma_kernel<BT, 128>, tma_block_smem<BT, 128>(), 128};
-        case 160: return {fg_block_tma_kernel<BT, 160>, tma_block_smem<BT, 160>(), 160};
-        case 192: return {fg_block_tma_kernel<BT, 192>, tma_block_smem<BT, 192>(), 192};
-        case 224: return {fg_block_tma_kernel<BT, 224>, tma_block_smem<BT, 224>(), 224};
-        default: return {fg_block_tma_kernel<BT, 256>, tma_block_smem<BT, 256>(), 256};
+        case 128: return {fg_block_tma_kernel<BT, 128, ST>, tma_block_smem<BT, 128, ST>(), 128};
+        case 192: return {fg_block_tma_kernel<BT, 192, ST>, tma_block_smem<BT, 192, ST>(), 192};
+        case 224: return {fg_block_tma_kernel<BT, 224, ST>, tma_block_smem<BT, 224, ST>(), 224};
+        default: return {fg_block_tma_kernel<BT, 256, ST>, tma_block_smem<BT, 256, ST>(), 256};
     }
 }
 
@@ -968,7 +975,8 @@ BlockVariant block_variant(int tp) {
 // 224 instead of 256 tiles of 256 that leave 40 SMs half idle.
 BlockVariant choose_block_variant(const fg_plan* p) {
     static const char* force = getenv("FGB200_BLOCK_TP");
-    const int cands[5] = {256, 224, 192, 160, 128};
+    const int cands[4] = {256, 224, 192, 128};
+    const bool staged = p->B == 1 && p->blkcoef_dev;
     BlockVariant best = {nullptr, 0, 0};
     int64_t best_cost = INT64_MAX;
     for (int tp : cands) {
@@ -977,7 +985,8 @@ BlockVariant choose_block_variant(const fg_plan* p) {
         const int64_t cost = ((tiles + sm_count() - 1) / sm_count()) * tp;
         if (cost < best_cost) {
             best_cost = cost;
-            best = p->tblock == 16 ? block_variant<16>(tp) : block_variant<8>(tp);
+            best = p->tblock == 16 ? (staged ? block_variant<16, true>(tp) : block_variant<16, false>(tp))
+                                   : (staged ? block_variant<8, true>(tp) : block_variant<8, false>(tp));
         }
     }
     return best;

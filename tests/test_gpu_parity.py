@@ -338,9 +338,14 @@ def test_persistent_multi_pass_ensemble(fg):
     dts = (0.2 * (1 / (n - 1)) ** 2) ** (1 / gam)
     cfg = fg.FieldConfig(initial=u0, dx=1 / (n - 1), gamma=gam, dt=dts, n_steps=steps,
                          strategy=fg.AdaptiveMemory(4), batched=True, snapshot_every=40)
-    pers = fg.run_field(cfg, flags=4)
+    pers = fg.run_field(cfg, flags=4, tblock=0)
     plain = fg.run_field(cfg, flags=0, tblock=0)
     for (_, a), (_, b) in zip(pers.snapshots, plain.snapshots):
+        assert np.array_equal(a, b)
+    # with temporal blocking: one cooperative launch per block == per-step PDL launches
+    pers_b = fg.run_field(cfg, flags=4, tblock=16)
+    pdl_b = fg.run_field(cfg, flags=2, tblock=16)
+    for (_, a), (_, b) in zip(pers_b.snapshots, pdl_b.snapshots):
         assert np.array_equal(a, b)
     idx = [0, 1, 1499, 2999]
     ref = fo.run(fo.OracleProblem(u0=u0[idx], gamma=gam[idx], dt=dts[idx], alpha=1.0, dx=1 / (n - 1),
