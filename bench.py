@@ -251,7 +251,12 @@ def run_ours(args) -> None:
     n_pts = prob.batch * prob.n_m
     hist_bytes = 8 * terms
     single_bytes, exec_bytes = execution_bytes(prob, st.tblock)
-    launches = n_steps + ((n_steps + st.tblock - 1) // st.tblock if st.tblock else 0)
+    # our kernels per run: every step, plus a coefficient kernel (single member)
+    # and a block kernel for every temporal block after the first (which starts
+    # from P = 0, a memset)
+    n_blocks = (n_steps + st.tblock - 1) // st.tblock if st.tblock else 0
+    per_block = 2 if prob.batch == 1 else 1
+    launches = n_steps + per_block * max(0, n_blocks - 1)
     stream = torch.cuda.current_stream(dev)
 
     def one_run():
