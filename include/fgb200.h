@@ -87,8 +87,10 @@ typedef struct fg_plan {
     int64_t horizon_max;         /* host copy of max(horizon_dev) (0 = unknown)    */
     int32_t tblock;              /* temporal blocking factor: 0 (off), 8 or 16     */
     int32_t reserved2;
-    double* P_dev;               /* [tblock][B*ms] scratch for blocked partial sums */
-    double* blkcoef_dev;         /* [h_slices][20] scratch, single-member blocking   */
+    double* P_dev;               /* [2][tblock][B*ms] scratch for blocked partial sums:
+                                    block kb0 uses buffer (kb0 / tblock) & 1        */
+    double* blkcoef_dev;         /* [2][h_slices][20] scratch, single-member blocking:
+                                    block kb0 uses buffer (kb0 / tblock) & 1        */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of
@@ -151,7 +153,10 @@ int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
  *                      cannot be co-resident);
  *   FG_RUN_PDL         per-step launches with programmatic dependent launch;
  *   FG_RUN_GRAPH       per-step launches captured into one CUDA graph.
- * All modes produce bitwise-identical results. */
+ * All modes produce bitwise-identical results.  With temporal blocking the
+ * per-step modes run each block's main block-kernel launch on a library-owned
+ * low-priority side stream, forked from and joined back into `stream` inside
+ * the call (FGB200_BLOCK_OVERLAP=0 disables it; results are unchanged). */
 #define FG_RUN_GRAPH 1
 #define FG_RUN_PDL 2
 #define FG_RUN_PERSISTENT 4
@@ -172,8 +177,10 @@ int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count);
 
 /* Temporal blocking building block (normally driven by fg_run): write into
- * plan->P_dev the partial sums of steps kb0..kb0+bt-1 over history slices
- * t < kb0 (bt <= plan->tblock).  Exposed for testing the block kernel alone. */
+ * buffer (kb0 / tblock) & 1 of plan->P_dev the partial sums of steps
+ * kb0..kb0+bt-1 over history slices t < kb0 (bt <= plan->tblock), as the main
+ * launch (t < kb0 - tblock) followed by the tail launch (the rest).  Exposed
+ * for testing the block kernel alone. */
 int fg_block_partials(const fg_plan* plan, int64_t kb0, int32_t bt, void* stream);
 
 /* Launch geometry fg_step would use: CTAs, threads per CTA, split factor. */

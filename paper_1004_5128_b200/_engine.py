@@ -185,6 +185,31 @@ def recent_entries(kind: str, k: int, param: float, horizon: int, mmax: int) -> 
     return n
 
 
+def block_launch_bytes(p: Problem, tblock: int) -> list[tuple[int, int, int]]:
+    """(kb0, bt, algorithmic bytes) of every block-kernel launch of one run.
+
+    A launch reads the union of its steps' old slices (t < kb0) once and writes
+    bt partial-sum slices; the first block (kb0 = 0) has no old slices and is a
+    memset, not a launch.
+    """
+    L = _lib.load()
+    out = C.c_int64(0)
+    base = int(p.param) if p.kind == "adaptive" else 0
+    members = range(p.batch) if p.kind == "short" else [0]
+    scale = p.n_m * 8 * (1 if p.kind == "short" else p.batch)
+    n = int(p.n_steps)
+    res = []
+    for kb0 in range(tblock, n, tblock):
+        bt = min(tblock, n - kb0)
+        slices = 0
+        for b in members:
+            hz = short_horizon(p.param, float(p.dt[b])) if p.kind == "short" else 0
+            _lib.check(L.fg_block_union(_lib.MEM_KINDS[p.kind], kb0, bt, base, hz, C.byref(out)))
+            slices += out.value + bt
+        res.append((kb0, bt, slices * scale))
+    return res
+
+
 def execution_bytes(p: Problem, tblock: int) -> tuple[int, int]:
     """(single-pass algorithmic bytes, bytes of the algorithm as executed) for one run.
 
@@ -251,7 +276,9 @@ class Stepper:
         slice_elems = B * self.ms
         self.snap_steps = snapshot_steps(n, p.cadence) if snapshots else []
         pool_slices = max(0, len([s for s in self.snap_steps if s > 0]))
-        dev_bytes = ((n + 1) + 2 + pool_slices) * slice_elems * 8 + B * (n + 1) * 8
+        tb = default_tblock() if tblock is None else int(tblock)
+        p_slices = 2 * tb if tb and n > tb else 0
+        dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         free, _total = torch.cuda.mem_get_info(self.device)
         free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
         if dev_bytes > free:
@@ -305,14 +332,15 @@ class Stepper:
         plan.status_dev = self.status.data_ptr()
         plan.snap_slot_dev = self.snap_slot.data_ptr() if self.snap_slot is not None else None
         plan.horizon_max = max(hz) if p.kind == "short" else 0
-        tb = default_tblock() if tblock is None else int(tblock)
         self.P = None
         if tb and n > tb:
-            self.P = torch.empty((tb, slice_elems), **f64)
+            # two buffers: block j's steps read one while block j+1's main launch
+            # fills the other (fg_run's side-stream pipeline)
+            self.P = torch.empty((2, tb, slice_elems), **f64)
             plan.tblock = tb
             plan.P_dev = self.P.data_ptr()
             if B == 1:  # per-block coefficient rows shared by all tiles
-                self.blkcoef = torch.empty((n + 1, 20), **f64)
+                self.blkcoef = torch.empty((2, n + 1, 20), **f64)  # two blocks in flight
                 plan.blkcoef_dev = self.blkcoef.data_ptr()
         self.tblock = int(plan.tblock)
         self.plan = plan
@@ -323,6 +351,10 @@ class Stepper:
         self._p_block: int | None = None  # block whose partial sums P holds
 
     # ---------------------------------------------------------------- driving --
+    def block_partials(self, kb0: int):
+        """View of the partial-sum buffer that holds the block starting at kb0."""
+        return self.P[(kb0 // self.tblock) & 1]
+
     def reset(self, u0_dev) -> None:
         """Rewind to step 0 from a device-resident padded u^0 (benchmark re-runs)."""
         self.u[0].copy_(u0_dev)

@@ -30,6 +30,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -62,6 +63,7 @@ constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit loa
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
+constexpr int kMaxTBlock = 16;  // largest temporal-blocking factor
 
 // ---------------------------------------------------------------- PTX helpers ---
 
@@ -186,6 +188,10 @@ struct StepArgs {
     int32_t blocked;       // temporal blocking: slices t < kb0 come from P
     int64_t kb0;           // first step of the current block
     const double* P;       // [tblock][B*ms] block partial sums (fg_block_kernel)
+    // blocked mode: schedule weight of offset m (1 <= m <= bb) in the schedule of
+    // step kb0+bb, 0 if absent — the only entries a blocked step still sums
+    // itself, host-evaluated so the step kernel builds no schedule at all
+    uint8_t rw[kMaxTBlock][kMaxTBlock];
 };
 
 // Number of schedule entries with offset m <= mmax (entries ascend in m).
@@ -201,7 +207,7 @@ __device__ __forceinline__ int64_t entries_upto(const FgSeg* s, int n, int64_t m
 
 
 template <int NDIM, int REACT, int S>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __grid_constant__ StepArgs a) {
     constexpr int kCols = (kThreads / 32) / S;   // warps across a tile
     constexpr int TP = kCols * 32 * kVec;        // points per tile
     constexpr int kLanes = kCols * 32;           // split-0 threads (one point pair each)
@@ -223,106 +229,155 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const Ste
     const bool multi = a.k1 - a.k0 > 1;
 
     for (int64_t k = a.k0; k < a.k1; ++k) {
-        // ================= A: schedule + old slices (m >= 2) =================
-        for (int i = tid; i < a.passes * kLanes; i += kThreads) s_acc[i] = make_double2(0.0, 0.0);
-        if (tid == 0) {
-            int n = fg_segments(a.kind, k, a.base, a.hz_max, segs);
-            int64_t acc = 0;
-            for (int i = 0; i < n; ++i) {
-                seg_first[i] = acc;
-                acc += segs[i].count;
-            }
-            seg_first[n] = acc;
-            s_nseg = n;
-            // temporal blocking: entries with m > bb (slices t < kb0) are already
-            // summed into P by fg_block_kernel; only m <= bb remain for this step
-            s_lim = a.blocked ? entries_upto(segs, n, k - a.kb0) : acc;
-        }
-        __syncthreads();
-        const int nseg = s_nseg;
-        const int64_t len = seg_first[nseg];
-        const int64_t lim = s_lim;
         const int64_t bb = k - a.kb0;
-        // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
-        // m = 1 whenever the schedule has it.  Both depend on step k-1's output
-        // and are summed in phase C; entries from 2 on read slices t <= k-2.
-        const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
-        const int64_t w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
-        const bool has_m1 = len >= 2 && m1 == 1 && (!a.blocked || bb >= 1);
-        const int64_t old = (len >= 2 && m1 == 1) ? 2 : 1;
-
-        for (int64_t c0 = old; c0 < lim; c0 += kChunk) {
-            const int cn = (int)((lim - c0) < kChunk ? (lim - c0) : kChunk);
-            for (int e = tid; e < cn; e += kThreads) {
-                const int64_t j = c0 + e;
-                int si = 0;
-                while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
-                const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
-                s_t[e] = (int32_t)(k - m);
-                s_w[e] = (int32_t)segs[si].stride;
-            }
-            int64_t cur_member = -1;
+        int64_t len, w1;   // schedule length (kinds 0/2), weight of m = 1
+        bool has_m1;
+        if (S == 1 && a.blocked) {
+            w1 = bb >= 1 ? a.rw[bb][1] : 0;
+            has_m1 = w1 != 0;
+            len = k + 1;  // only used for the m = 1 test below (k >= bb >= 1)
+            // ====== A (temporal blocking): recent slices 2 <= m <= bb only ======
+            // Everything older is in P[bb]; the weights come from the host table,
+            // so there is no schedule, no shared staging and no CTA barrier here.
+            // Same entry order and rounding as the general path below.
             for (int p = 0; p < a.passes; ++p) {
                 const int tile = blockIdx.x + p * G;
                 if (tile >= a.total_tiles) break;
                 const int64_t b = tile / a.tpm;
-                if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
-                    __syncthreads();
-                    const double* psi_b = a.psi + b * a.psi_stride;
-                    for (int e = tid; e < cn; e += kThreads)
-                        s_c[e] = __dmul_rn((double)s_w[e], __ldg(psi_b + (k - s_t[e])));
-                    __syncthreads();
-                    cur_member = b;
-                }
-                int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
-                if (len_b > lim) len_b = lim;
-                const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
                 const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
                 double acc0 = 0.0, acc1 = 0.0;
-                if (q < a.n_m) {
-                    const double* hbase = a.H + b * a.ms + q;
-                    for (int e0 = split; e0 < cnb; e0 += S * kUnroll) {
-                        double2 v[kUnroll];
-                        double c[kUnroll];
+                if (q < a.n_m && bb >= 2) {
+                    const double* hbase = a.H + b * a.ms + q + k * a.slice_stride;
+                    const double* psi_b = a.psi + b * a.psi_stride;
+                    const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
+                    const uint8_t* row = a.rw[bb];
+                    constexpr int kR = REACT ? 4 : 5;  // recent slices in flight per round (no spills)
+#pragma unroll 1
+                    for (int m0 = 2; m0 <= mmax; m0 += kR) {
+                        double2 v[kR];
+                        double c[kR];
 #pragma unroll
-                        for (int u = 0; u < kUnroll; ++u) {
-                            const int e = e0 + u * S;
-                            if (e < cnb) {
-                                v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
-                                c[u] = s_c[e];
+                        for (int u = 0; u < kR; ++u) {
+                            const int m = m0 + u;
+                            const int w = (m <= mmax) ? row[m] : 0;
+                            if (w) {
+                                v[u] = ld_stream(hbase - (int64_t)m * a.slice_stride);
+                                c[u] = __dmul_rn((double)w, __ldg(psi_b + m));
                             } else {
                                 v[u] = make_double2(0.0, 0.0);
                                 c[u] = 0.0;
                             }
                         }
 #pragma unroll
-                        for (int u = 0; u < kUnroll; ++u) {
+                        for (int u = 0; u < kR; ++u) {
                             acc0 = fma(c[u], v[u].x, acc0);
                             acc1 = fma(c[u], v[u].y, acc1);
                         }
                     }
                 }
-                if (S > 1) {
-                    if (split > 0) s_part[(split - 1) * kLanes + slot] = make_double2(acc0, acc1);
-                    __syncthreads();
-                    if (split == 0) {
+                s_acc[p * kLanes + slot] = make_double2(__dadd_rn(0.0, acc0), __dadd_rn(0.0, acc1));
+            }
+        } else {
+            // ================= A: schedule + old slices (m >= 2) =================
+            for (int i = tid; i < a.passes * kLanes; i += kThreads) s_acc[i] = make_double2(0.0, 0.0);
+            if (tid == 0) {
+                int n = fg_segments(a.kind, k, a.base, a.hz_max, segs);
+                int64_t acc = 0;
+                for (int i = 0; i < n; ++i) {
+                    seg_first[i] = acc;
+                    acc += segs[i].count;
+                }
+                seg_first[n] = acc;
+                s_nseg = n;
+                // temporal blocking: entries with m > bb (slices t < kb0) are already
+                // summed into P by fg_block_kernel; only m <= bb remain for this step
+                s_lim = a.blocked ? entries_upto(segs, n, k - a.kb0) : acc;
+            }
+            __syncthreads();
+            const int nseg = s_nseg;
+            len = seg_first[nseg];
+            const int64_t lim = s_lim;
+            // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
+            // m = 1 whenever the schedule has it.  Both depend on step k-1's output
+            // and are summed in phase C; entries from 2 on read slices t <= k-2.
+            const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
+            w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
+            has_m1 = len >= 2 && m1 == 1 && (!a.blocked || bb >= 1);
+            const int64_t old = (len >= 2 && m1 == 1) ? 2 : 1;
+
+            for (int64_t c0 = old; c0 < lim; c0 += kChunk) {
+                const int cn = (int)((lim - c0) < kChunk ? (lim - c0) : kChunk);
+                for (int e = tid; e < cn; e += kThreads) {
+                    const int64_t j = c0 + e;
+                    int si = 0;
+                    while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
+                    const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
+                    s_t[e] = (int32_t)(k - m);
+                    s_w[e] = (int32_t)segs[si].stride;
+                }
+                int64_t cur_member = -1;
+                for (int p = 0; p < a.passes; ++p) {
+                    const int tile = blockIdx.x + p * G;
+                    if (tile >= a.total_tiles) break;
+                    const int64_t b = tile / a.tpm;
+                    if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
+                        __syncthreads();
+                        const double* psi_b = a.psi + b * a.psi_stride;
+                        for (int e = tid; e < cn; e += kThreads)
+                            s_c[e] = __dmul_rn((double)s_w[e], __ldg(psi_b + (k - s_t[e])));
+                        __syncthreads();
+                        cur_member = b;
+                    }
+                    int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+                    if (len_b > lim) len_b = lim;
+                    const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
+                    const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
+                    double acc0 = 0.0, acc1 = 0.0;
+                    if (q < a.n_m) {
+                        const double* hbase = a.H + b * a.ms + q;
+                        for (int e0 = split; e0 < cnb; e0 += S * kUnroll) {
+                            double2 v[kUnroll];
+                            double c[kUnroll];
 #pragma unroll
-                        for (int s = 1; s < S; ++s) {
-                            const double2 pp = s_part[(s - 1) * kLanes + slot];
-                            acc0 = __dadd_rn(acc0, pp.x);
-                            acc1 = __dadd_rn(acc1, pp.y);
+                            for (int u = 0; u < kUnroll; ++u) {
+                                const int e = e0 + u * S;
+                                if (e < cnb) {
+                                    v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
+                                    c[u] = s_c[e];
+                                } else {
+                                    v[u] = make_double2(0.0, 0.0);
+                                    c[u] = 0.0;
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < kUnroll; ++u) {
+                                acc0 = fma(c[u], v[u].x, acc0);
+                                acc1 = fma(c[u], v[u].y, acc1);
+                            }
                         }
                     }
-                    __syncthreads();
+                    if (S > 1) {
+                        if (split > 0) s_part[(split - 1) * kLanes + slot] = make_double2(acc0, acc1);
+                        __syncthreads();
+                        if (split == 0) {
+#pragma unroll
+                            for (int s = 1; s < S; ++s) {
+                                const double2 pp = s_part[(s - 1) * kLanes + slot];
+                                acc0 = __dadd_rn(acc0, pp.x);
+                                acc1 = __dadd_rn(acc1, pp.y);
+                            }
+                        }
+                        __syncthreads();
+                    }
+                    if (split == 0) {
+                        double2& r = s_acc[p * kLanes + slot];
+                        r.x = __dadd_rn(r.x, acc0);
+                        r.y = __dadd_rn(r.y, acc1);
+                    }
                 }
-                if (split == 0) {
-                    double2& r = s_acc[p * kLanes + slot];
-                    r.x = __dadd_rn(r.x, acc0);
-                    r.y = __dadd_rn(r.y, acc1);
-                }
+                __syncthreads();  // s_t / s_w / s_c are refilled by the next chunk
             }
-            __syncthreads();  // s_t / s_w / s_c are refilled by the next chunk
-        }
+        }  // general A phase
 
         // ================= dependency on step k-1 =================
         if (multi) {
@@ -435,8 +490,10 @@ struct BlockArgs {
     const int64_t* horizon;
     int64_t slice_stride, ms, psi_stride, base;
     int64_t kb0;
+    int64_t t_begin, t_end;  // slices summed by this launch: [t_begin, t_end) ∩ [t_lo, kb0)
     int32_t bt;
     int32_t n_m, kind, tpm, total_tiles;
+    int32_t accumulate;      // P += D (tail launch) instead of P = D
     const double* gcoef;  // single-member blocks: precomputed coefficient rows (or NULL)
 };
 
@@ -491,6 +548,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
 }
 
+// History rows are streamed once per block: mark them evict-first in L2 so the
+// stream does not push out what the concurrently running steps touch (fields,
+// partial sums, the recent slices), which would turn their L2 hits into HBM
+// misses queued behind the stream.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -506,8 +582,11 @@ __host__ __device__ constexpr int row_pitch() { return TP + 4; }
 template <int BT>
 __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 
+#ifndef FG_STAGED_RING
+#define FG_STAGED_RING 6
+#endif
 template <bool STAGED>
-__host__ __device__ constexpr int ring_stages() { return STAGED ? 6 : 4; }
+__host__ __device__ constexpr int ring_stages() { return STAGED ? FG_STAGED_RING : 4; }
 
 template <int BT, int TP, bool STAGED>
 size_t tma_block_smem() {
@@ -592,7 +671,11 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     const int64_t hz = a.kind == 1 ? a.horizon[mem] : 0;
     // oldest slice any step of the block can reach: short memory stops at kb0 - H
     const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
-    const int64_t n_sl = a.kb0 - t_lo;
+    // this launch's share of [t_lo, kb0): the main launch takes everything but the
+    // previous block's slices, the tail launch those
+    const int64_t ts = a.t_begin > t_lo ? a.t_begin : t_lo;
+    const int64_t te = a.t_end;
+    const int64_t n_sl = te > ts ? te - ts : 0;
     const int64_t n_st = (n_sl + kE - 1) / kE;
 
     if (tid == 0) {
@@ -609,15 +692,17 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     if (warp == NW) {  // ---- producer: lane 0 drives the bulk-copy ring
         if (lane == 0) {
             const double* src0 = a.H + mem * a.ms + q0;
+            const uint64_t pol = l2_evict_first_policy();
             for (int64_t g = 0; g < n_st; ++g) {
                 const int s = (int)(g % kStages);
                 if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                const int64_t t0 = t_lo + g * kE;
-                const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
+                const int64_t t0 = ts + g * kE;
+                const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
                 const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
                 mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
                 for (int e = 0; e < nr; ++e)
-                    bulk_g2s(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes, &full[s]);
+                    bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
+                                  &full[s], pol);
                 if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - t_lo) * CP, cbytes, &full[s]);
             }
         }
@@ -634,7 +719,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
     const int ngroups = TP / BT;  // threads per step column when filling the table
     for (int64_t g = 0; g < n_st; ++g) {
-        const int64_t t0 = t_lo + g * kE;
+        const int64_t t0 = ts + g * kE;
         if (!staged && (g * kE) % kCH == 0) {
             // ensemble path: coefficient table for slices t0 .. t0+kCH-1 — zero it,
             // then scatter w·ψ_b(m) over every schedule segment (no per-slice search)
@@ -644,7 +729,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
             const int bb = tid % BT, grp = tid / BT;
             if (bb < a.bt) {
                 const int64_t k = a.kb0 + bb;
-                const int64_t t_hi = (t0 + kCH - 1 < a.kb0 - 1) ? t0 + kCH - 1 : a.kb0 - 1;
+                const int64_t t_hi = (t0 + kCH - 1 < te - 1) ? t0 + kCH - 1 : te - 1;
                 const int64_t m_lo = k - t_hi, m_hi = k - t0;  // offsets mapping into this table
                 const FgSeg* sg = segs + bb * kBlkSegs;
                 for (int si = 0; si < nseg[bb]; ++si) {
@@ -662,7 +747,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         }
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
-        const int nr = (int)((a.kb0 - t0) < kE ? (a.kb0 - t0) : kE);
+        const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
         const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
         const double* cs = (staged ? coef + (size_t)s * kE * CP : coef + ((g * kE) % kCH) * CP) + fr;
         // all fragments of the stage into registers first ...
@@ -706,7 +791,14 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
             const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
-            if (q < a.n_m) st_pair(pout + bb * a.slice_stride + 8 * j, d[i][j][0], d[i][j][1]);
+            if (q >= a.n_m) continue;
+            double* o = pout + bb * a.slice_stride + 8 * j;
+            if (a.accumulate) {
+                const double2 old = ld_cg2(o);
+                st_pair(o, __dadd_rn(old.x, d[i][j][0]), __dadd_rn(old.y, d[i][j][1]));
+            } else {
+                st_pair(o, d[i][j][0], d[i][j][1]);
+            }
         }
     }
 }
@@ -916,6 +1008,50 @@ StepArgs make_args(const fg_plan* p, int s) {
     return a;
 }
 
+// Partial sums of the block of steps [kb0, kb0+bt) over slices t < kb0 live in
+// P[(kb0 / tblock) & 1] (two buffers: the next block's main launch fills one while
+// the current block's steps read the other).
+double* block_P(const fg_plan* p, int64_t kb0) {
+    return p->P_dev + ((kb0 / p->tblock) & 1) * (int64_t)p->tblock * p->B * p->ms;
+}
+
+// Coefficient rows of block kb0 (single member): buffer (kb0 / tblock) & 1 of
+// blkcoef_dev, h_slices rows of kCoefRow doubles each, so the next block's main
+// launch can rebuild its rows while this block's tail launch still reads these.
+constexpr int kCoefRow = 20;  // >= coef_pitch<16>()
+double* block_coef(const fg_plan* p, int64_t kb0) {
+    return p->blkcoef_dev + ((kb0 / p->tblock) & 1) * p->h_slices * kCoefRow;
+}
+
+// Recent-weight rows of a temporal block: a.rw[k-kb0][m] = weight of offset m in
+// the schedule of step k (1 <= m <= k-kb0), for k in [k0, k1).
+void fill_recent(StepArgs& a, const fg_plan* p, int64_t kb0, int64_t k0, int64_t k1) {
+    FgSeg segs[FG_MAX_SEGS];
+    for (int64_t k = k0; k < k1; ++k) {
+        const int64_t bb = k - kb0;
+        const int n = fg_segments(p->kind, k, p->base, a.hz_max, segs);
+        for (int64_t m = 1; m <= bb && n > 0; ++m) a.rw[bb][m] = (uint8_t)fg_seg_weight(segs, n, m);
+    }
+}
+
+// Ask for the largest shared-memory carveout for every kernel of the pipeline so
+// an SM running two block-kernel CTAs (2 x ~94 KB) is configured with room left
+// for a step-kernel CTA; with the default choice the SM is carved to just fit the
+// block CTAs and the concurrent steps wait for them to drain.
+int prefer_max_smem(const void* fn) {
+    static std::mutex mu;
+    static std::vector<const void*> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const void* f : done)
+        if (f == fn) return FG_OK;
+    if (int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 (int)cudaSharedmemCarveoutMaxShared),
+                            "smem carveout"))
+        return rc;
+    done.push_back(fn);
+    return FG_OK;
+}
+
 size_t acc_smem(int s, int passes) { return (size_t)passes * (size_t)((kThreads / 32) / s) * 32 * sizeof(double2); }
 
 // One step, one launch; grid = one CTA per tile.  kb0 >= 0: temporal-blocking
@@ -933,9 +1069,11 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
     if (kb0 >= 0) {
         a.blocked = 1;
         a.kb0 = kb0;
-        a.P = p->P_dev;
+        a.P = block_P(p, kb0);
+        fill_recent(a, p, kb0, k, k + 1);
     }
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
+    if (int rc = prefer_max_smem((const void*)kern)) return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.total_tiles, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
@@ -992,18 +1130,11 @@ BlockVariant choose_block_variant(const fg_plan* p) {
     return best;
 }
 
-// Partial sums of the block of steps [kb0, kb0+bt) over slices t < kb0.
-int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
-    if (kb0 <= 0) {  // nothing older than the block: P = 0
-        return cuda_check(cudaMemsetAsync(p->P_dev, 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
-                          "P reset");
-    }
-    const BlockVariant v = choose_block_variant(p);
-    if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
+BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& v) {
     BlockArgs a;
     memset(&a, 0, sizeof a);
     a.H = p->H_dev;
-    a.P = p->P_dev;
+    a.P = block_P(p, kb0);
     a.psi = p->psi_dev;
     a.horizon = p->horizon_dev;
     a.slice_stride = p->B * p->ms;
@@ -1016,25 +1147,93 @@ int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     a.kind = p->kind;
     a.tpm = (int32_t)((p->n_m + v.tp - 1) / v.tp);
     a.total_tiles = (int32_t)(a.tpm * p->B);
+    a.gcoef = (p->B == 1 && p->blkcoef_dev) ? block_coef(p, kb0) : nullptr;
+    return a;
+}
+
+// main launch: P = Σ over slices t < kb0 - tblock (all but the previous block's),
+// after the block's coefficient rows (single member).  Everything it reads is
+// final once step kb0 - tblock - 1 ... kb0 - 1's predecessor block is done, so
+// fg_run issues it on a side stream while the previous block's steps run.
+int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
+    if (kb0 <= 0) {  // nothing older than the block: P = 0
+        return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
+                          "P reset");
+    }
+    const BlockVariant v = choose_block_variant(p);
+    if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
+    BlockArgs a = block_args(p, kb0, bt, v);
+    a.t_begin = 0;
+    a.t_end = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
         return rc;
-    if (p->B == 1 && p->blkcoef_dev) {  // coefficient rows computed once for all tiles
+    if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
+    if (a.gcoef) {  // coefficient rows computed once for all tiles (main and tail)
         const int64_t hz_host = p->kind == 1 ? p->horizon_max : 0;  // B == 1: the member's horizon
         const int64_t t_lo = (p->kind == 1 && kb0 - hz_host > 0) ? kb0 - hz_host : 0;
         const size_t cp = p->tblock == 16 ? coef_pitch<16>() : coef_pitch<8>();
-        if (int rc = cuda_check(cudaMemsetAsync(p->blkcoef_dev, 0, (size_t)(kb0 - t_lo) * cp * sizeof(double), st),
+        if (int rc = cuda_check(cudaMemsetAsync(const_cast<double*>(a.gcoef), 0, (size_t)(kb0 - t_lo) * cp * sizeof(double), st),
                                 "coefficient rows reset"))
             return rc;
         if (p->tblock == 16)
-            fg_block_coef_kernel<16><<<bt, 256, 0, st>>>(a, p->blkcoef_dev);
+            fg_block_coef_kernel<16><<<bt, 256, 0, st>>>(a, const_cast<double*>(a.gcoef));
         else
-            fg_block_coef_kernel<8><<<bt, 256, 0, st>>>(a, p->blkcoef_dev);
+            fg_block_coef_kernel<8><<<bt, 256, 0, st>>>(a, const_cast<double*>(a.gcoef));
         if (int rc = cuda_check(cudaGetLastError(), "fg_block_coef launch")) return rc;
-        a.gcoef = p->blkcoef_dev;
     }
     v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
+}
+
+// tail launch: P += Σ over the previous block's slices [kb0 - tblock, kb0), in
+// stream order after that block's last step and this block's main launch.
+int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
+    if (kb0 <= 0) return FG_OK;
+    const BlockVariant v = choose_block_variant(p);
+    if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
+    BlockArgs a = block_args(p, kb0, bt, v);
+    a.t_begin = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
+    a.t_end = kb0;
+    a.accumulate = 1;
+    v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
+    return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
+}
+
+// FGB200_BLOCK_OVERLAP=0 turns the side-stream pipeline off (same results).
+bool overlap_enabled() {
+    const char* e = getenv("FGB200_BLOCK_OVERLAP");
+    return !(e && e[0] == '0');
+}
+
+// Per-thread side stream (lowest priority, so the latency-bound steps win SM
+// slots as they free) and its fork/join events, on the current device.
+int side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
+    static thread_local int dev = -1;
+    static thread_local cudaStream_t side = nullptr;
+    static thread_local cudaEvent_t ef = nullptr, ej[2] = {nullptr, nullptr};
+    int cur = 0;
+    if (int rc = cuda_check(cudaGetDevice(&cur), "cudaGetDevice")) return rc;
+    if (!side || dev != cur) {
+        int least = 0, greatest = 0;
+        if (int rc = cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range")) return rc;
+        if (int rc = cuda_check(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least), "side stream"))
+            return rc;
+        if (int rc = cuda_check(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming), "fork event")) return rc;
+        for (int i = 0; i < 2; ++i)
+            if (int rc = cuda_check(cudaEventCreateWithFlags(&ej[i], cudaEventDisableTiming), "join event")) return rc;
+        dev = cur;
+    }
+    *s = side;
+    *fork = ef;
+    join[0] = ej[0];
+    join[1] = ej[1];
+    return FG_OK;
+}
+
+int launch_block(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
+    if (int rc = launch_block_main(p, kb0, bt, st)) return rc;
+    return launch_block_tail(p, kb0, bt, st);
 }
 
 // Persistent geometry: G co-resident CTAs, `passes` tiles each.  Returns 0 and
@@ -1070,7 +1269,8 @@ int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cu
     if (kb0 >= 0) {  // the steps of one temporal block
         a.blocked = 1;
         a.kb0 = kb0;
-        a.P = p->P_dev;
+        a.P = block_P(p, kb0);
+        fill_recent(a, p, kb0, k0, k1);
     }
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
     const size_t smem = acc_smem(s, passes);
@@ -1257,7 +1457,33 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
     int rc = FG_OK;
     const int64_t tb = p->tblock;
     const int64_t n_total = p->psi_stride - 1 < p->h_slices - 1 ? p->psi_stride - 1 : p->h_slices - 1;
+    auto block_len = [&](int64_t kb) {
+        const int64_t left = n_total - kb;
+        return (int)(left < tb ? (left > 0 ? left : 1) : tb);
+    };
+    // Temporal-blocking pipeline: block j+1's main launch (all
+    // slices older than block j) runs on a side stream while block j's steps run
+    // here; the side stream forks after block j's tail launch and joins before
+    // block j+1's tail.  Same launches and arithmetic as without the overlap.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    if (tb && overlap_enabled()) {
+        if (int r = side_stream(&side, &ev_fork, ev_join)) {
+            if (graph) {
+                cudaGraph_t dead = nullptr;
+                cudaStreamEndCapture(cap, &dead);
+                if (dead) cudaGraphDestroy(dead);
+            }
+            return r;
+        }
+    }
+    int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
     bool after_block = false;
+    // TRACE (temporary)
+    const bool trace = getenv("FGB200_TRACE") != nullptr;
+    struct TB { int64_t kb; cudaEvent_t s_end_prev, s_tail0, s_tail1, b0, b1; };
+    std::vector<TB> tr;
+    auto mkev = []() { cudaEvent_t e; cudaEventCreate(&e); return e; };
     for (int64_t k = k0; k < k1 && rc == FG_OK; ++k) {
         double* snap = nullptr;
         if (si < n_snap && snap_steps[si] == k + 1) {
@@ -1270,14 +1496,63 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
             // blocks are aligned to multiples of tb, so a run split into several
             // fg_run calls recomputes the same partial sums (deterministic)
             if (k == kb0 || (k == k0 && !(flags & FG_RUN_CONTINUE))) {
-                const int64_t left = n_total - kb0;
-                rc = launch_block(p, kb0, (int)(left < tb ? (left > 0 ? left : 1) : tb), cap);
+                TB cur = {kb0, nullptr, nullptr, nullptr, nullptr, nullptr};
+                if (trace) { cur.s_end_prev = mkev(); cudaEventRecord(cur.s_end_prev, cap); }
+                // fork first: the next block's main launch only needs slices
+                // t < kb0 (final here) and its own P / coefficient buffers, so it
+                // queues on the side stream right behind this block's main launch
+                const int64_t nk = kb0 + tb;
+                const bool fork_next = side && nk < k1;
+                if (fork_next) {
+                    rc = cuda_check(cudaEventRecord(ev_fork, cap), "fork record");
+                    if (rc == FG_OK) rc = cuda_check(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+                    if (trace) { cur.b0 = mkev(); cudaEventRecord(cur.b0, side); }
+                    if (rc == FG_OK) rc = launch_block_main(p, nk, block_len(nk), side);
+                    if (trace) { cur.b1 = mkev(); cudaEventRecord(cur.b1, side); }
+                    if (rc == FG_OK) rc = cuda_check(cudaEventRecord(ev_join[(nk / tb) & 1], side), "join record");
+                    if (rc != FG_OK) break;
+                }
+                if (main_on_side == kb0) {
+                    rc = cuda_check(cudaStreamWaitEvent(cap, ev_join[(kb0 / tb) & 1], 0), "join side stream");
+                } else {
+                    rc = launch_block_main(p, kb0, block_len(kb0), cap);
+                }
+                main_on_side = fork_next ? nk : -1;
+                if (trace) { cur.s_tail0 = mkev(); cudaEventRecord(cur.s_tail0, cap); }
+                if (rc == FG_OK) rc = launch_block_tail(p, kb0, block_len(kb0), cap);
+                if (trace) { cur.s_tail1 = mkev(); cudaEventRecord(cur.s_tail1, cap); }
                 if (rc != FG_OK) break;
                 after_block = true;
+                if (trace) tr.push_back(cur);
             }
         }
         rc = launch_single(p, k, snap, cap, pdl && k > k0 && !after_block, pdl, kb0);
         after_block = false;
+    }
+    if (trace && !tr.empty()) {
+        cudaEvent_t fin = mkev();
+        cudaEventRecord(fin, cap);
+        cudaStreamSynchronize(cap);
+        cudaDeviceSynchronize();
+        FILE* f = fopen(getenv("FGB200_TRACE"), "a");
+        float t;
+        for (size_t i = 0; i < tr.size(); ++i) {
+            const TB& c = tr[i];
+            float tail = 0, steps = 0, mainr = 0, wait = 0, lag = 0;
+            cudaEventElapsedTime(&tail, c.s_tail0, c.s_tail1);
+            cudaEvent_t nxt = i + 1 < tr.size() ? tr[i + 1].s_end_prev : fin;
+            cudaEventElapsedTime(&steps, c.s_tail1, nxt);
+            if (c.b0) { cudaEventElapsedTime(&mainr, c.b0, c.b1); cudaEventElapsedTime(&lag, c.s_end_prev, c.b0); }
+            cudaEventElapsedTime(&wait, c.s_end_prev, c.s_tail0);
+            cudaEventElapsedTime(&t, tr[0].s_end_prev, c.s_end_prev);
+            fprintf(f, "%lld t=%.1f wait=%.1f tail=%.1f steps=%.1f main_next=%.1f lag=%.1f\n", (long long)c.kb, t * 1e3,
+                    wait * 1e3, tail * 1e3, steps * 1e3, mainr * 1e3, lag * 1e3);
+        }
+        fclose(f);
+    }
+    if (main_on_side >= 0) {  // error path: never leave the side stream unjoined
+        const int r2 = cuda_check(cudaStreamWaitEvent(cap, ev_join[(main_on_side / tb) & 1], 0), "join side stream");
+        if (rc == FG_OK) rc = r2;
     }
     if (graph) {
         cudaError_t e = cudaStreamEndCapture(cap, &g);

@@ -53,7 +53,8 @@ def launches(path: str) -> dict:
     cnt = collections.Counter()
     unit = rows[0][2] if rows else ""
     for name, v, _ in rows:
-        short = name.split("(")[0].split("<")[0]
+        short = name.replace("void ", "").replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+        short = short.split("(")[0].split("<")[0]
         tot[short] += v
         cnt[short] += 1
     total = sum(tot.values())

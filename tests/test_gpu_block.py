@@ -49,11 +49,11 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     L = _lib.load()
     _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
     torch.cuda.synchronize()
-    P1 = st.P[:bt].clone()
+    P1 = st.block_partials(kb0)[:bt].clone()
     for rep in range(5):
         _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
         torch.cuda.synchronize()
-        bad = (P1 != st.P[:bt]).nonzero()
+        bad = (P1 != st.block_partials(kb0)[:bt]).nonzero()
         assert bad.numel() == 0, f"rerun {rep} differs at {bad.shape[0]} places, first {bad[:8].tolist()}"
     n = int(np.prod(shape))
     H = st.H[:kb0, :n].cpu().numpy()

@@ -411,13 +411,18 @@ def test_temporal_blocking_matches_goldens(fg, golden, name, tblock):
 
 
 @pytest.mark.parametrize("name", ["c2_small", "batch_short", "3d_sat_full"])
-def test_temporal_blocking_modes_bitwise(fg, golden, name):
-    """Blocked runs are identical across launch modes, across runs split into
-    several launches (partial sums continued or recomputed), and reruns."""
+def test_temporal_blocking_modes_bitwise(fg, golden, name, monkeypatch):
+    """Blocked runs are identical across launch modes (side-stream pipeline on
+    and off, persistent), across runs split into several launches (partial sums
+    continued or recomputed), and reruns."""
     cfg = _any_field_config(fg, golden, name)
     ref = fg.run_field(cfg, flags=0, tblock=16)
-    for kw in (dict(flags=1), dict(flags=2), dict(flags=3), dict(progress_every=7), dict(progress_every=16)):
+    for kw in (dict(flags=1), dict(flags=2), dict(flags=3), dict(flags=4), dict(progress_every=7),
+               dict(progress_every=16), dict(flags=2, overlap="0"), dict(flags=1, overlap="0")):
+        kw = dict(kw)
+        monkeypatch.setenv("FGB200_BLOCK_OVERLAP", kw.pop("overlap", "1"))
         got = fg.run_field(cfg, tblock=16, **kw)
+        assert len(got.snapshots) == len(ref.snapshots)
         for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
             assert s0 == s1 and np.array_equal(a0, a1), kw
 
