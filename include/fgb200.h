@@ -89,7 +89,7 @@ typedef struct fg_plan {
     int32_t reserved2;
     double* P_dev;               /* [2][tblock][B*ms] scratch for blocked partial sums:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
-    double* blkcoef_dev;         /* [2][h_slices][20] scratch, single-member blocking:
+    double* blkcoef_dev;         /* [2][h_slices][36] scratch, single-member blocking:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
 } fg_plan;
 
@@ -167,6 +167,15 @@ int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
 int fg_run(const fg_plan* plan, int64_t k0, int64_t k1,
            const int64_t* snap_steps, int64_t n_snap, double* snap_pool_dev,
            int32_t flags, void* stream);
+
+/* fg_run plus snapshot streaming: when snap_pool_host (pinned host memory,
+ * same layout as snap_pool_dev) is non-NULL, each snapshot is copied there on a
+ * library-owned copy stream as soon as the launch that wrote it is done, so the
+ * device-to-host traffic overlaps the following steps; the copies are joined
+ * into `stream` before the call returns (a sync of `stream` covers them). */
+int fg_run_ex(const fg_plan* plan, int64_t k0, int64_t k1,
+              const int64_t* snap_steps, int64_t n_snap, double* snap_pool_dev,
+              double* snap_pool_host, int32_t flags, void* stream);
 
 /* Stream-synchronous read of status_dev[0] (first non-finite step). */
 int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);

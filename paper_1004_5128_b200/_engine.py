@@ -340,7 +340,7 @@ class Stepper:
             plan.tblock = tb
             plan.P_dev = self.P.data_ptr()
             if B == 1:  # per-block coefficient rows shared by all tiles
-                self.blkcoef = torch.empty((2, n + 1, 20), **f64)  # two blocks in flight
+                self.blkcoef = torch.empty((2, n + 1, _lib.FG_COEF_ROW), **f64)  # two blocks in flight
                 plan.blkcoef_dev = self.blkcoef.data_ptr()
         self.tblock = int(plan.tblock)
         self.plan = plan
@@ -371,9 +371,10 @@ class Stepper:
     def advance(self, k1: int, *, flags: int | None = None, stream_snapshots: bool = False) -> None:
         """Launch steps self.k .. k1-1 (asynchronous, stream-ordered).
 
-        With ``stream_snapshots`` the launch sequence is cut at every snapshot
-        step and each snapshot is copied to pinned host memory on a side stream
-        while the following steps run (the D2H hides under the stepping loop).
+        With ``stream_snapshots`` every snapshot is copied to pinned host memory
+        by the library (fg_run_ex) on its copy stream as soon as the step that
+        produced it is done, overlapping the following steps; the copies are
+        joined into the current stream.
         """
         k0 = self.k
         if k1 <= k0:
@@ -381,20 +382,17 @@ class Stepper:
         snaps = [s for s in self.snap_steps if s > 0]
         arr = (C.c_int64 * max(1, len(snaps)))(*snaps)
         pool = self.pool.data_ptr() if self.pool is not None else None
+        host = None
+        if stream_snapshots and self.pool is not None:
+            if self.pool_host is None:
+                self.pool_host = self.torch.empty(self.pool.shape, dtype=self.torch.float64, pin_memory=True)
+            host = self.pool_host.data_ptr()
+            self.copied.update(i for i, s in enumerate(snaps) if k0 < s <= k1)
         fl = self.flags if flags is None else flags
-        st = _lib.stream_handle()
-        cuts = [(i, s) for i, s in enumerate(snaps) if k0 < s <= k1] if stream_snapshots and snaps else []
-        start = k0
-        for i, s in cuts + [(None, k1)]:
-            if start >= s:
-                continue
-            _lib.check(self.L.fg_run(C.byref(self.plan), start, s, arr, len(snaps), pool,
-                                     fl | self._continue_flag(start), st), "fg_run")
-            if self.tblock:
-                self._p_block = (s - 1) - (s - 1) % self.tblock
-            if i is not None:
-                self._copy_out(i)
-            start = s
+        _lib.check(self.L.fg_run_ex(C.byref(self.plan), k0, k1, arr, len(snaps), pool, host,
+                                    fl | self._continue_flag(k0), _lib.stream_handle()), "fg_run_ex")
+        if self.tblock:
+            self._p_block = (k1 - 1) - (k1 - 1) % self.tblock
         self.k = k1
 
     def _continue_flag(self, start: int) -> int:
@@ -402,18 +400,6 @@ class Stepper:
         if self.tblock and self._p_block is not None and start - start % self.tblock == self._p_block:
             return _lib.FG_RUN_CONTINUE
         return 0
-
-    def _copy_out(self, i: int) -> None:
-        torch = self.torch
-        if self.pool_host is None:
-            self.pool_host = torch.empty(self.pool.shape, dtype=torch.float64, pin_memory=True)
-            self.copy_stream = torch.cuda.Stream(self.device)
-        ev = torch.cuda.Event()
-        ev.record()
-        self.copy_stream.wait_event(ev)
-        with torch.cuda.stream(self.copy_stream):
-            self.pool_host[i].copy_(self.pool[i], non_blocking=True)
-        self.copied.add(i)
 
     def run(self, progress_every: int = 0) -> float:
         """Run every step; return the loop's wall time (solver.py:248-257 semantics)."""
@@ -463,8 +449,7 @@ class Stepper:
         later = [s for s in self.snap_steps if s > 0]
         self.d2h_bytes = 0
         if later:
-            if self.copy_stream is not None:
-                self.copy_stream.synchronize()
+            torch.cuda.current_stream(self.device).synchronize()  # joins the library's snapshot copies
             missing = [i for i in range(len(later)) if i not in self.copied]
             if self.pool_host is None:
                 self.pool_host = torch.empty(self.pool.shape, dtype=torch.float64, pin_memory=True)

@@ -22,6 +22,7 @@ FG_RUN_PDL = 2
 FG_RUN_PERSISTENT = 4
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
+FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
 REACTIONS = {"linear": 0, "saturating": 1}
@@ -29,7 +30,7 @@ REACTIONS = {"linear": 0, "saturating": 1}
 # every symbol include/fgb200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
     "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
-    "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_status",
+    "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_run_ex", "fg_status",
     "fg_step_geometry", "fg_block_union", "fg_block_partials",
 )
 
@@ -94,6 +95,7 @@ def _declare(L):
         "fg_stencil": (C.c_int, [plan, vp, vp, vp]),
         "fg_step": (C.c_int, [plan, i64, vp, vp]),
         "fg_run": (C.c_int, [plan, i64, i64, _p64, i64, vp, i32, vp]),
+        "fg_run_ex": (C.c_int, [plan, i64, i64, _p64, i64, vp, vp, i32, vp]),
         "fg_status": (C.c_int, [plan, _p64, vp]),
         "fg_step_geometry": (C.c_int, [plan, _p64, _p32, _p32]),
         "fg_block_union": (C.c_int, [i32, i64, i32, i64, i64, _p64]),

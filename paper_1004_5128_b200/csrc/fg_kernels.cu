@@ -63,7 +63,7 @@ constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit loa
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
-constexpr int kMaxTBlock = 16;  // largest temporal-blocking factor
+constexpr int kMaxTBlock = 32;  // largest temporal-blocking factor
 
 // ---------------------------------------------------------------- PTX helpers ---
 
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
             for (int i = tid; i < kCH * CP; i += TP) coef[i] = 0.0;
             asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
             const int bb = tid % BT, grp = tid / BT;
-            if (bb < a.bt) {
+            if (bb < a.bt && grp < ngroups) {
                 const int64_t k = a.kb0 + bb;
                 const int64_t t_hi = (t0 + kCH - 1 < te - 1) ? t0 + kCH - 1 : te - 1;
                 const int64_t m_lo = k - t_hi, m_hi = k - t0;  // offsets mapping into this table
@@ -904,8 +904,8 @@ int validate_plan(const fg_plan* p) {
         return fail(FG_ERR_ARG, "plan has a NULL device pointer");
     if (p->split != 0 && p->split != 1 && p->split != 2 && p->split != 4 && p->split != 8)
         return fail(FG_ERR_ARG, "split must be 0, 1, 2, 4 or 8");
-    if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16)
-        return fail(FG_ERR_ARG, "tblock must be 0, 8 or 16");
+    if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16 && p->tblock != 24 && p->tblock != 32)
+        return fail(FG_ERR_ARG, "tblock must be 0, 8, 16, 24 or 32");
     if (p->tblock && !p->P_dev) return fail(FG_ERR_ARG, "temporal blocking needs P_dev");
     if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
         FgSeg s[FG_MAX_SEGS];
@@ -1018,7 +1018,7 @@ double* block_P(const fg_plan* p, int64_t kb0) {
 // Coefficient rows of block kb0 (single member): buffer (kb0 / tblock) & 1 of
 // blkcoef_dev, h_slices rows of kCoefRow doubles each, so the next block's main
 // launch can rebuild its rows while this block's tail launch still reads these.
-constexpr int kCoefRow = 20;  // >= coef_pitch<16>()
+constexpr int kCoefRow = 36;  // >= coef_pitch<kMaxTBlock>()
 double* block_coef(const fg_plan* p, int64_t kb0) {
     return p->blkcoef_dev + ((kb0 / p->tblock) & 1) * p->h_slices * kCoefRow;
 }
@@ -1123,8 +1123,12 @@ BlockVariant choose_block_variant(const fg_plan* p) {
         const int64_t cost = ((tiles + sm_count() - 1) / sm_count()) * tp;
         if (cost < best_cost) {
             best_cost = cost;
-            best = p->tblock == 16 ? (staged ? block_variant<16, true>(tp) : block_variant<16, false>(tp))
-                                   : (staged ? block_variant<8, true>(tp) : block_variant<8, false>(tp));
+            switch (p->tblock) {
+                case 8: best = staged ? block_variant<8, true>(tp) : block_variant<8, false>(tp); break;
+                case 24: best = staged ? block_variant<24, true>(tp) : block_variant<24, false>(tp); break;
+                case 32: best = staged ? block_variant<32, true>(tp) : block_variant<32, false>(tp); break;
+                default: best = staged ? block_variant<16, true>(tp) : block_variant<16, false>(tp); break;
+            }
         }
     }
     return best;
@@ -1172,14 +1176,17 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (a.gcoef) {  // coefficient rows computed once for all tiles (main and tail)
         const int64_t hz_host = p->kind == 1 ? p->horizon_max : 0;  // B == 1: the member's horizon
         const int64_t t_lo = (p->kind == 1 && kb0 - hz_host > 0) ? kb0 - hz_host : 0;
-        const size_t cp = p->tblock == 16 ? coef_pitch<16>() : coef_pitch<8>();
+        const size_t cp = (size_t)p->tblock + 4;  // coef_pitch<tblock>()
         if (int rc = cuda_check(cudaMemsetAsync(const_cast<double*>(a.gcoef), 0, (size_t)(kb0 - t_lo) * cp * sizeof(double), st),
                                 "coefficient rows reset"))
             return rc;
-        if (p->tblock == 16)
-            fg_block_coef_kernel<16><<<bt, 256, 0, st>>>(a, const_cast<double*>(a.gcoef));
-        else
-            fg_block_coef_kernel<8><<<bt, 256, 0, st>>>(a, const_cast<double*>(a.gcoef));
+        double* rows = const_cast<double*>(a.gcoef);
+        switch (p->tblock) {
+            case 8: fg_block_coef_kernel<8><<<bt, 256, 0, st>>>(a, rows); break;
+            case 24: fg_block_coef_kernel<24><<<bt, 256, 0, st>>>(a, rows); break;
+            case 32: fg_block_coef_kernel<32><<<bt, 256, 0, st>>>(a, rows); break;
+            default: fg_block_coef_kernel<16><<<bt, 256, 0, st>>>(a, rows); break;
+        }
         if (int rc = cuda_check(cudaGetLastError(), "fg_block_coef launch")) return rc;
     }
     v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
@@ -1228,6 +1235,25 @@ int side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
     *fork = ef;
     join[0] = ej[0];
     join[1] = ej[1];
+    return FG_OK;
+}
+
+// Per-thread device-to-host copy stream for fg_run_ex snapshots.
+int copy_stream(cudaStream_t* s, cudaEvent_t* ev, cudaEvent_t* join) {
+    static thread_local int dev = -1;
+    static thread_local cudaStream_t cs = nullptr;
+    static thread_local cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int cur = 0;
+    if (int rc = cuda_check(cudaGetDevice(&cur), "cudaGetDevice")) return rc;
+    if (!cs || dev != cur) {
+        if (int rc = cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream")) return rc;
+        if (int rc = cuda_check(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming), "copy event")) return rc;
+        if (int rc = cuda_check(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "copy event")) return rc;
+        dev = cur;
+    }
+    *s = cs;
+    *ev = e0;
+    *join = e1;
     return FG_OK;
 }
 
@@ -1387,6 +1413,11 @@ int fg_step(const fg_plan* p, int64_t k, double* snap, void* stream) {
 
 int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, int64_t n_snap, double* pool,
            int32_t flags, void* stream) {
+    return fg_run_ex(p, k0, k1, snap_steps, n_snap, pool, nullptr, flags, stream);
+}
+
+int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, int64_t n_snap, double* pool,
+              double* host_pool, int32_t flags, void* stream) {
     if (int rc = validate_plan(p)) return rc;
     if (k0 < 0 || k1 < k0 || k1 > p->h_slices || k1 > p->psi_stride)
         return fail(FG_ERR_ARG, "fg_run: step range [%lld, %lld) outside history capacity %lld", (long long)k0,
@@ -1395,9 +1426,12 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
     if (k1 == k0) return FG_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int s = choose_split(p);
+    const int64_t tb = p->tblock;
 
+    // ---- persistent launches: one cooperative grid per run (or per temporal block)
+    int G = 0, passes = 0;
+    bool persistent = false;
     if ((flags & FG_RUN_PERSISTENT) && k1 - k0 > 1) {
-        int G = 0, passes = 0;
         if (int rc = persistent_geometry(p, s, &G, &passes)) return rc;
         bool snaps_ok = true;
         if (n_snap > 0) {
@@ -1415,28 +1449,12 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
                 if (int rc = cuda_check(cudaStreamSynchronize(st), "snapshot map sync")) return rc;
             }
         }
-        if (G > 0 && snaps_ok) {
-            double* pl = n_snap > 0 ? pool : nullptr;
-            if (!p->tblock) return launch_persistent(p, k0, k1, pl, st, G, passes, s);
-            // temporal blocking: per block, the block kernel then one cooperative
-            // launch running the block's steps with the split grid barrier
-            const int64_t tb = p->tblock;
-            const int64_t n_total = p->psi_stride - 1 < p->h_slices - 1 ? p->psi_stride - 1 : p->h_slices - 1;
-            for (int64_t kb = k0 - k0 % tb; kb < k1; kb += tb) {
-                const int64_t ks = kb > k0 ? kb : k0, ke = kb + tb < k1 ? kb + tb : k1;
-                if (ks == kb || !(flags & FG_RUN_CONTINUE)) {
-                    const int64_t left = n_total - kb;
-                    if (int rc = launch_block(p, kb, (int)(left < tb ? (left > 0 ? left : 1) : tb), st)) return rc;
-                }
-                if (int rc = launch_persistent(p, ks, ke, pl, st, G, passes, s, kb)) return rc;
-            }
-            return FG_OK;
-        }
-        // fall through to per-step launches
+        persistent = G > 0 && snaps_ok;  // else fall back to per-step launches
     }
+    double* ppool = n_snap > 0 ? pool : nullptr;
 
     const int pdl = (flags & FG_RUN_PDL) ? 1 : 0;
-    const bool graph = (flags & FG_RUN_GRAPH) != 0;
+    const bool graph = (flags & FG_RUN_GRAPH) != 0 && !persistent;
     const int64_t slice = p->B * p->ms;
     // Capture into a private stream (the legacy default stream cannot capture),
     // then replay the graph on the caller's stream.
@@ -1455,103 +1473,105 @@ int fg_run(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_steps, 
     int64_t si = 0;
     while (si < n_snap && snap_steps[si] <= k0) ++si;
     int rc = FG_OK;
-    const int64_t tb = p->tblock;
-    const int64_t n_total = p->psi_stride - 1 < p->h_slices - 1 ? p->psi_stride - 1 : p->h_slices - 1;
-    auto block_len = [&](int64_t kb) {
-        const int64_t left = n_total - kb;
-        return (int)(left < tb ? (left > 0 ? left : 1) : tb);
-    };
-    // Temporal-blocking pipeline: block j+1's main launch (all
-    // slices older than block j) runs on a side stream while block j's steps run
-    // here; the side stream forks after block j's tail launch and joins before
-    // block j+1's tail.  Same launches and arithmetic as without the overlap.
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
-    if (tb && overlap_enabled()) {
-        if (int r = side_stream(&side, &ev_fork, ev_join)) {
-            if (graph) {
-                cudaGraph_t dead = nullptr;
-                cudaStreamEndCapture(cap, &dead);
-                if (dead) cudaGraphDestroy(dead);
-            }
-            return r;
-        }
+
+    // snapshots to host: each one is copied on a library copy stream as soon as
+    // the launch that produced it is done, overlapping the following steps
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t cev = nullptr, cjoin = nullptr;
+    if (host_pool && n_snap > 0) {
+        if (int r = copy_stream(&cstream, &cev, &cjoin)) rc = r;
     }
-    int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
-    bool after_block = false;
-    // TRACE (temporary)
-    const bool trace = getenv("FGB200_TRACE") != nullptr;
-    struct TB { int64_t kb; cudaEvent_t s_end_prev, s_tail0, s_tail1, b0, b1; };
-    std::vector<TB> tr;
-    auto mkev = []() { cudaEvent_t e; cudaEventCreate(&e); return e; };
-    for (int64_t k = k0; k < k1 && rc == FG_OK; ++k) {
-        double* snap = nullptr;
-        if (si < n_snap && snap_steps[si] == k + 1) {
-            snap = pool + si * slice;
-            ++si;
+    auto copy_out = [&](int64_t i0, int64_t i1) {  // snapshots [i0, i1) are complete on `cap`
+        if (!cstream || i1 <= i0) return (int)FG_OK;
+        if (int r = cuda_check(cudaEventRecord(cev, cap), "snapshot event")) return r;
+        if (int r = cuda_check(cudaStreamWaitEvent(cstream, cev, 0), "snapshot wait")) return r;
+        return cuda_check(cudaMemcpyAsync(host_pool + i0 * slice, pool + i0 * slice,
+                                          (size_t)(i1 - i0) * slice * sizeof(double), cudaMemcpyDeviceToHost, cstream),
+                          "snapshot copy");
+    };
+
+    // per-step launches of steps [ka, kz); first_after_block: the previous
+    // launch on `cap` was a block launch (no programmatic dependency on it)
+    auto steps = [&](int64_t ka, int64_t kz, int64_t kb0, bool first_after_block) {
+        for (int64_t k = ka; k < kz; ++k) {
+            double* snap = nullptr;
+            const int64_t i = si;
+            if (si < n_snap && snap_steps[si] == k + 1) {
+                snap = pool + si * slice;
+                ++si;
+            }
+            const bool wait = pdl && k > k0 && !(k == ka && first_after_block);
+            if (int r = launch_single(p, k, snap, cap, wait, pdl, kb0)) return r;
+            if (snap)
+                if (int r = copy_out(i, i + 1)) return r;
         }
-        int64_t kb0 = -1;
-        if (tb) {
-            kb0 = k - k % tb;
+        return (int)FG_OK;
+    };
+    // persistent launch over [ka, kz): its snapshots are copied after it
+    auto persistent_steps = [&](int64_t ka, int64_t kz, int64_t kb0) {
+        if (int r = kb0 >= 0 ? launch_persistent(p, ka, kz, ppool, cap, G, passes, s, kb0)
+                             : launch_persistent(p, ka, kz, ppool, cap, G, passes, s))
+            return r;
+        const int64_t i0 = si;
+        while (si < n_snap && snap_steps[si] <= kz) ++si;
+        return copy_out(i0, si);
+    };
+
+    if (rc != FG_OK) {
+    } else if (!tb) {
+        rc = persistent ? persistent_steps(k0, k1, -1) : steps(k0, k1, -1, false);
+    } else {
+        // Temporal-blocking pipeline.  Block j (steps K_j ..
+        // K_j+tb-1) needs P_j = main_j (slices t < K_{j-1}) + tail_j (slices
+        // K_{j-1} .. K_j-1).  main_{j+1} only reads slices t < K_j, final once
+        // block j starts, and writes its own P / coefficient buffers, so it is
+        // forked onto a low-priority side stream at block j's start and runs
+        // behind main_j while block j's tail and steps run here; block j+1 then
+        // joins it.  Same launches and arithmetic with or without the overlap.
+        const int64_t n_total = p->psi_stride - 1 < p->h_slices - 1 ? p->psi_stride - 1 : p->h_slices - 1;
+        auto block_len = [&](int64_t kb) {
+            const int64_t left = n_total - kb;
+            return (int)(left < tb ? (left > 0 ? left : 1) : tb);
+        };
+        cudaStream_t side = nullptr;
+        cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+        if (overlap_enabled()) rc = side_stream(&side, &ev_fork, ev_join);
+        int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
+        for (int64_t kb = k0 - k0 % tb; kb < k1 && rc == FG_OK; kb += tb) {
+            const int64_t ks = kb > k0 ? kb : k0, ke = kb + tb < k1 ? kb + tb : k1;
             // blocks are aligned to multiples of tb, so a run split into several
             // fg_run calls recomputes the same partial sums (deterministic)
-            if (k == kb0 || (k == k0 && !(flags & FG_RUN_CONTINUE))) {
-                TB cur = {kb0, nullptr, nullptr, nullptr, nullptr, nullptr};
-                if (trace) { cur.s_end_prev = mkev(); cudaEventRecord(cur.s_end_prev, cap); }
-                // fork first: the next block's main launch only needs slices
-                // t < kb0 (final here) and its own P / coefficient buffers, so it
-                // queues on the side stream right behind this block's main launch
-                const int64_t nk = kb0 + tb;
+            const bool start = ks == kb || !(flags & FG_RUN_CONTINUE);
+            if (start) {
+                const int64_t nk = kb + tb;
                 const bool fork_next = side && nk < k1;
                 if (fork_next) {
                     rc = cuda_check(cudaEventRecord(ev_fork, cap), "fork record");
                     if (rc == FG_OK) rc = cuda_check(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
-                    if (trace) { cur.b0 = mkev(); cudaEventRecord(cur.b0, side); }
                     if (rc == FG_OK) rc = launch_block_main(p, nk, block_len(nk), side);
-                    if (trace) { cur.b1 = mkev(); cudaEventRecord(cur.b1, side); }
                     if (rc == FG_OK) rc = cuda_check(cudaEventRecord(ev_join[(nk / tb) & 1], side), "join record");
                     if (rc != FG_OK) break;
                 }
-                if (main_on_side == kb0) {
-                    rc = cuda_check(cudaStreamWaitEvent(cap, ev_join[(kb0 / tb) & 1], 0), "join side stream");
-                } else {
-                    rc = launch_block_main(p, kb0, block_len(kb0), cap);
-                }
+                if (main_on_side == kb)
+                    rc = cuda_check(cudaStreamWaitEvent(cap, ev_join[(kb / tb) & 1], 0), "join side stream");
+                else
+                    rc = launch_block_main(p, kb, block_len(kb), cap);
                 main_on_side = fork_next ? nk : -1;
-                if (trace) { cur.s_tail0 = mkev(); cudaEventRecord(cur.s_tail0, cap); }
-                if (rc == FG_OK) rc = launch_block_tail(p, kb0, block_len(kb0), cap);
-                if (trace) { cur.s_tail1 = mkev(); cudaEventRecord(cur.s_tail1, cap); }
+                if (rc == FG_OK) rc = launch_block_tail(p, kb, block_len(kb), cap);
                 if (rc != FG_OK) break;
-                after_block = true;
-                if (trace) tr.push_back(cur);
             }
+            rc = persistent ? persistent_steps(ks, ke, kb) : steps(ks, ke, kb, start);
         }
-        rc = launch_single(p, k, snap, cap, pdl && k > k0 && !after_block, pdl, kb0);
-        after_block = false;
-    }
-    if (trace && !tr.empty()) {
-        cudaEvent_t fin = mkev();
-        cudaEventRecord(fin, cap);
-        cudaStreamSynchronize(cap);
-        cudaDeviceSynchronize();
-        FILE* f = fopen(getenv("FGB200_TRACE"), "a");
-        float t;
-        for (size_t i = 0; i < tr.size(); ++i) {
-            const TB& c = tr[i];
-            float tail = 0, steps = 0, mainr = 0, wait = 0, lag = 0;
-            cudaEventElapsedTime(&tail, c.s_tail0, c.s_tail1);
-            cudaEvent_t nxt = i + 1 < tr.size() ? tr[i + 1].s_end_prev : fin;
-            cudaEventElapsedTime(&steps, c.s_tail1, nxt);
-            if (c.b0) { cudaEventElapsedTime(&mainr, c.b0, c.b1); cudaEventElapsedTime(&lag, c.s_end_prev, c.b0); }
-            cudaEventElapsedTime(&wait, c.s_end_prev, c.s_tail0);
-            cudaEventElapsedTime(&t, tr[0].s_end_prev, c.s_end_prev);
-            fprintf(f, "%lld t=%.1f wait=%.1f tail=%.1f steps=%.1f main_next=%.1f lag=%.1f\n", (long long)c.kb, t * 1e3,
-                    wait * 1e3, tail * 1e3, steps * 1e3, mainr * 1e3, lag * 1e3);
+        if (main_on_side >= 0) {  // error path: never leave the side stream unjoined
+            const int r2 =
+                cuda_check(cudaStreamWaitEvent(cap, ev_join[(main_on_side / tb) & 1], 0), "join side stream");
+            if (rc == FG_OK) rc = r2;
         }
-        fclose(f);
     }
-    if (main_on_side >= 0) {  // error path: never leave the side stream unjoined
-        const int r2 = cuda_check(cudaStreamWaitEvent(cap, ev_join[(main_on_side / tb) & 1], 0), "join side stream");
+
+    if (cstream) {  // join the copies: a sync of `stream` covers the host snapshots
+        int r2 = cuda_check(cudaEventRecord(cjoin, cstream), "copy join record");
+        if (r2 == FG_OK) r2 = cuda_check(cudaStreamWaitEvent(cap, cjoin, 0), "copy join");
         if (rc == FG_OK) rc = r2;
     }
     if (graph) {

@@ -394,7 +394,7 @@ BLOCK_CASES = ["small", "point_full", "point_short100", "point_adaptive3", "poin
                "c2_small_full", "c2_small_short", "spread_g09_adaptive4"] + ND_CASES
 
 
-@pytest.mark.parametrize("tblock", [8, 16])
+@pytest.mark.parametrize("tblock", [8, 16, 24, 32])
 @pytest.mark.parametrize("name", BLOCK_CASES)
 def test_temporal_blocking_matches_goldens(fg, golden, name, tblock):
     """One history pass feeding `tblock` steps reproduces the reference (≤1e-10)."""
