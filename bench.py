@@ -234,24 +234,28 @@ def time_block_stage(st, prob, stream) -> dict:
     from paper_1004_5128_b200._engine import block_launch_bytes
 
     L = _lib.load()
-    blocks = block_launch_bytes(prob, st.tblock)
+    blocks = block_launch_bytes(prob, st.tblock, with_flops=True)
     if not blocks:
         return None
     h = C.c_void_p(_lib.stream_handle(stream))
     plan = C.byref(st.plan)
-    for kb0, bt, _ in blocks[-4:]:  # warm (code, smem config)
+    for kb0, bt, _, _ in blocks[-4:]:  # warm (code, smem config)
         _lib.check(L.fg_block_partials(plan, kb0, bt, h), "fg_block_partials")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
-    for kb0, bt, _ in blocks:
+    for kb0, bt, _, _ in blocks:
         _lib.check(L.fg_block_partials(plan, kb0, bt, h), "fg_block_partials")
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    nbytes = sum(b for _, _, b in blocks)
+    nbytes = sum(b[2] for b in blocks)
+    flops = sum(b[3] for b in blocks)
+    fp64_peak = 37.0e12  # measured DMMA m8n8k4 rate, profiles/fp64_rates.txt
     return {"launches": len(blocks), "total_ms": ms, "avg_launch_us": ms * 1e3 / len(blocks),
             "alg_bytes_per_launch": nbytes / len(blocks), "alg_bytes_total": nbytes,
+            "alg_flops_total": flops, "fp64_tflops": flops / (ms * 1e-3) / 1e12,
+            "fp64_frac": flops / (ms * 1e-3) / fp64_peak, "fp64_peak_tflops": fp64_peak / 1e12,
             "share_of_run": None}
 
 

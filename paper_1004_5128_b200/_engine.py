@@ -59,10 +59,20 @@ def default_flags() -> int:
     return _lib.FG_RUN_PDL
 
 
-def default_tblock() -> int:
-    """Temporal blocking factor (0 = off).  One history pass feeds 16 steps."""
+def default_tblock(p: "Problem | None" = None) -> int:
+    """Temporal blocking factor (0 = off): one history pass feeds this many steps.
+
+    Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
+    full / adaptive runs are fastest at 32 (the block kernel turns fp64-tensor
+    bound), short memory and ensembles (per-member coefficient tables built in
+    the CTA) at 24.
+    """
     env = os.environ.get("FGB200_TBLOCK")
-    return int(env) if env is not None else 16
+    if env is not None:
+        return int(env)
+    if p is None:
+        return 24
+    return 24 if (p.batch > 1 or p.kind == "short") else 32
 
 
 def round_up(n: int, m: int) -> int:
@@ -185,28 +195,38 @@ def recent_entries(kind: str, k: int, param: float, horizon: int, mmax: int) -> 
     return n
 
 
-def block_launch_bytes(p: Problem, tblock: int) -> list[tuple[int, int, int]]:
-    """(kb0, bt, algorithmic bytes) of every block-kernel launch of one run.
+def block_launch_bytes(p: Problem, tblock: int, with_flops: bool = False) -> list[tuple]:
+    """(kb0, bt, algorithmic bytes[, algorithmic flops]) of every block stage of one run.
 
-    A launch reads the union of its steps' old slices (t < kb0) once and writes
-    bt partial-sum slices; the first block (kb0 = 0) has no old slices and is a
-    memset, not a launch.
+    A block stage (main + tail launch) reads the union of its steps' old slices
+    (t < kb0) once and writes bt partial-sum slices; its flops are 2 per point
+    per old schedule entry (m > b for step kb0+b).  The first block (kb0 = 0)
+    has no old slices and is a memset, not a launch.
     """
     L = _lib.load()
     out = C.c_int64(0)
     base = int(p.param) if p.kind == "adaptive" else 0
+    kind = _lib.MEM_KINDS[p.kind]
     members = range(p.batch) if p.kind == "short" else [0]
-    scale = p.n_m * 8 * (1 if p.kind == "short" else p.batch)
+    scale = p.n_m * (1 if p.kind == "short" else p.batch)
     n = int(p.n_steps)
+    hzs = {b: (short_horizon(p.param, float(p.dt[b])) if p.kind == "short" else 0) for b in members}
     res = []
     for kb0 in range(tblock, n, tblock):
         bt = min(tblock, n - kb0)
         slices = 0
+        terms = 0
         for b in members:
-            hz = short_horizon(p.param, float(p.dt[b])) if p.kind == "short" else 0
-            _lib.check(L.fg_block_union(_lib.MEM_KINDS[p.kind], kb0, bt, base, hz, C.byref(out)))
+            hz = hzs[b]
+            _lib.check(L.fg_block_union(kind, kb0, bt, base, hz, C.byref(out)))
             slices += out.value + bt
-        res.append((kb0, bt, slices * scale))
+            if with_flops:
+                for bb in range(bt):
+                    k = kb0 + bb
+                    _lib.check(L.fg_schedule_len(kind, k, base, hz, C.byref(out)))
+                    terms += out.value - 1 - recent_entries(p.kind, k, p.param, hz, bb)
+        rec = (kb0, bt, slices * scale * 8)
+        res.append(rec + (2 * terms * scale,) if with_flops else rec)
     return res
 
 
@@ -276,7 +296,7 @@ class Stepper:
         slice_elems = B * self.ms
         self.snap_steps = snapshot_steps(n, p.cadence) if snapshots else []
         pool_slices = max(0, len([s for s in self.snap_steps if s > 0]))
-        tb = default_tblock() if tblock is None else int(tblock)
+        tb = default_tblock(p) if tblock is None else int(tblock)
         p_slices = 2 * tb if tb and n > tb else 0
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         free, _total = torch.cuda.mem_get_info(self.device)
