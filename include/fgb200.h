@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FGB200_ABI_VERSION 1
+#define FGB200_ABI_VERSION 2
 
 #define FG_OK 0
 #define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
@@ -89,8 +89,12 @@ typedef struct fg_plan {
     int32_t reserved2;
     double* P_dev;               /* [2][tblock][B*ms] scratch for blocked partial sums:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
-    double* blkcoef_dev;         /* [2][h_slices][36] scratch, single-member blocking:
+    double* blkcoef_dev;         /* [2][coef_rows][36] scratch, single-member blocking:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
+    double* Q_dev;               /* [q_rows][B*ms] scratch, single-member thinned
+                                    schedules: per-item partial sums (NULL: dense)  */
+    int64_t q_rows;
+    int64_t coef_rows;           /* rows per blkcoef buffer (0 = h_slices)          */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of

@@ -72,7 +72,12 @@ def default_tblock(p: "Problem | None" = None) -> int:
         return int(env)
     if p is None:
         return 24
-    return 24 if (p.batch > 1 or p.kind == "short") else 32
+    if p.batch > 1:
+        return 24
+    # a short memory at least as long as the run is the full schedule, and must
+    # give the full schedule's bits (reference property, test_covering_strategies)
+    truncating = p.kind == "short" and short_horizon(p.param, float(p.dt[0])) < int(p.n_steps)
+    return 24 if truncating else 32
 
 
 def round_up(n: int, m: int) -> int:
@@ -298,6 +303,8 @@ class Stepper:
         pool_slices = max(0, len([s for s in self.snap_steps if s > 0]))
         tb = default_tblock(p) if tblock is None else int(tblock)
         p_slices = 2 * tb if tb and n > tb else 0
+        if tb and n > tb and B == 1 and p.kind == "adaptive":
+            p_slices += tb * _lib.FG_MAX_ITEM_ROWS_PER_STEP  # Q
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         free, _total = torch.cuda.mem_get_info(self.device)
         free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
@@ -360,8 +367,16 @@ class Stepper:
             plan.tblock = tb
             plan.P_dev = self.P.data_ptr()
             if B == 1:  # per-block coefficient rows shared by all tiles
-                self.blkcoef = torch.empty((2, n + 1, _lib.FG_COEF_ROW), **f64)  # two blocks in flight
+                # two blocks in flight; rows for the tail, every slice of the main
+                # launch and the slices two strides' items share
+                rows = 2 * (n + 1) + 4 * tb
+                self.blkcoef = torch.empty((2, rows, _lib.FG_COEF_ROW), **f64)
                 plan.blkcoef_dev = self.blkcoef.data_ptr()
+                plan.coef_rows = rows
+                if p.kind == "adaptive":  # per-item partial sums of the thinned schedule
+                    plan.q_rows = tb * _lib.FG_MAX_ITEM_ROWS_PER_STEP
+                    self.Q = torch.empty((plan.q_rows, slice_elems), **f64)
+                    plan.Q_dev = self.Q.data_ptr()
         self.tblock = int(plan.tblock)
         self.plan = plan
         self.k = 0

@@ -12,6 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FGB200_LIB") or os.path.join(HERE, "_lib", "libfgb200.so")
 
+ABI_VERSION = 2  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
 FG_OK = 0
 FG_ERR_ARG = -1
 FG_ERR_CUDA = -2
@@ -23,6 +24,7 @@ FG_RUN_PERSISTENT = 4
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
+FG_MAX_ITEM_ROWS_PER_STEP = 8  # Q rows a step can own (kMaxQ in fg_kernels.cu)
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
 REACTIONS = {"linear": 0, "saturating": 1}
@@ -72,6 +74,9 @@ class FgPlan(C.Structure):
         ("reserved2", C.c_int32),
         ("P_dev", C.c_void_p),
         ("blkcoef_dev", C.c_void_p),
+        ("Q_dev", C.c_void_p),
+        ("q_rows", C.c_int64),
+        ("coef_rows", C.c_int64),
     ]
 
 
@@ -120,6 +125,8 @@ def load(path: str = LIB_PATH):
         except OSError as exc:  # pragma: no cover - environment specific
             raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
         _declare(L)
+        if L.fg_abi_version() != ABI_VERSION:
+            raise NativeLibraryError(f"{path} has ABI {L.fg_abi_version()}, this binding expects {ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 

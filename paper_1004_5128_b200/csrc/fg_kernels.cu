@@ -64,6 +64,7 @@ constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
 constexpr int kMaxTBlock = 32;  // largest temporal-blocking factor
+constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxTBlock + 4)
 
 // ---------------------------------------------------------------- PTX helpers ---
 
@@ -617,19 +618,20 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
     const int bb = blockIdx.x;
     const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
     const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
+    const int64_t ts = a.t_begin > t_lo ? a.t_begin : t_lo, te = a.t_end;  // rows t - ts, t in [ts, te)
     const int64_t k = a.kb0 + bb;
     if (threadIdx.x == 0) nseg = fg_segments(a.kind, k, a.base, hz, segs);
     __syncthreads();
     for (int si = 0; si < nseg; ++si) {
-        // entries m = m0 + i*stride with t = k - m in [t_lo, kb0), i.e. m >= bb+1
+        // entries m = m0 + i*stride with t = k - m in [ts, te)
         const int64_t m0 = segs[si].m0, st = segs[si].stride, cnt = segs[si].count;
-        const int64_t m_min = bb + 1, m_max = k - t_lo;
+        const int64_t m_min = k - te + 1, m_max = k - ts;
         if (m_max < m0 || m_min > m0 + (cnt - 1) * st) continue;
         const int64_t i0 = m_min > m0 ? (m_min - m0 + st - 1) / st : 0;
         const int64_t i1 = (m_max - m0) / st < cnt - 1 ? (m_max - m0) / st : cnt - 1;
         for (int64_t i = i0 + threadIdx.x; i <= i1; i += blockDim.x) {
             const int64_t m = m0 + i * st;
-            out[(k - m - t_lo) * CP + bb] = __dmul_rn((double)st, __ldg(a.psi + m));
+            out[(k - m - ts) * CP + bb] = __dmul_rn((double)st, __ldg(a.psi + m));
         }
     }
 }
@@ -703,7 +705,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
                 for (int e = 0; e < nr; ++e)
                     bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
                                   &full[s], pol);
-                if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - t_lo) * CP, cbytes, &full[s]);
+                if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
             }
         }
         return;
@@ -801,6 +803,246 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
             }
         }
     }
+}
+
+// ------------------------------------------- class-decomposed block stage ---
+// A thinned (adaptive) schedule samples offsets m with stride s inside each
+// interval, so in a block only the steps b with kb0+b-t ≡ m0 (mod s) use slice
+// t: the dense [BT x slices] coefficient tile above is mostly zeros (c2: ~1 in
+// 9 nonzero) and the fp64 tensor pipe, not HBM, bounds the main launch.  Here
+// the block's (step, slice) pairs of the main range are partitioned into
+// items = (stride s, residue t mod s): an item streams its slices t_first +
+// j*s (every slice of the block's union is read by exactly the items that use
+// it — one for most slices) and multiplies them with a dense coefficient tile
+// over only its own steps (≈ BT/s), so the work executed is the schedule's
+// terms rounded up to 8-step DMMA tiles.  Items write per-item partial rows
+// Q; a fixed-order reduction sums each step's rows into P (deterministic).
+// Full and short memory are one item (s = 1, every step) written to P directly.
+
+constexpr int kMaxItems = 112;
+constexpr int kMaxQ = 8;  // items a step may appear in (distinct strides)
+
+struct BlockItem {
+    int64_t t_first;
+    int32_t stride, n_slices;
+    int32_t coef_row;  // first coefficient row (kCoefRow doubles each) of this item
+    int32_t q_row;     // first Q row (direct mode: unused)
+    int32_t ncols;     // steps in the item; column c is step col2step[c]
+    uint8_t col2step[kMaxTBlock];
+};
+
+struct ItemTable {
+    int32_t n_items;
+    int32_t direct;  // one item holding every step in order: write P rows directly
+    int32_t accumulate;
+    int32_t pad;
+    BlockItem it[kMaxItems];
+    uint8_t nq[kMaxTBlock];           // Q rows of step b, summed in this order
+    int16_t q[kMaxTBlock][kMaxQ];
+};
+
+// Coefficient rows of every item: row (coef_row + j), column c =
+// w·ψ(kb0 + col2step[c] - t_j) when that offset is in step col2step[c]'s
+// schedule with weight w == the item's stride (the entry belongs to this
+// item), else 0; columns ncols..CP-1 are zero padding for the DMMA tiles.
+template <int BT>
+__global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
+                                    double* __restrict__ out) {
+    constexpr int CP = coef_pitch<BT>();
+    __shared__ FgSeg segs[BT][kBlkSegs];
+    __shared__ int nseg[BT];
+    const BlockItem& it = T.it[blockIdx.y];
+    const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
+    if (threadIdx.x < it.ncols) {
+        const int b = it.col2step[threadIdx.x];
+        nseg[threadIdx.x] = fg_segments(a.kind, a.kb0 + b, a.base, hz, segs[threadIdx.x], kBlkSegs);
+    }
+    __syncthreads();
+    const int64_t rows = it.n_slices;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * CP;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / CP;
+        const int c = (int)(e - j * CP);
+        double v = 0.0;
+        if (c < it.ncols) {
+            const int b = it.col2step[c];
+            const int64_t m = a.kb0 + b - (it.t_first + j * it.stride);
+            const int32_t w = fg_seg_weight(segs[c], nseg[c], m);
+            if (w == it.stride) v = __dmul_rn((double)w, __ldg(a.psi + m));
+        }
+        out[((int64_t)it.coef_row + j) * CP + c] = v;
+    }
+}
+
+// One ring stage of an item with MTE live M tiles: fragments of the stage's
+// kE slices into registers, release the slot (after the reads, see
+// fg_block_tma_kernel), then MTE x NT x 2 DMMAs.
+template <int MTE, int MT, int NT, int CP, int RP>
+__device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double* cs, const double* rs, int nr, int fk,
+                                           int lane, uint64_t* empty_s, double* sink_w) {
+    double af[kE / 4][MTE], bf[kE / 4][NT];
+    uint32_t xr = 0;
+#pragma unroll
+    for (int ks = 0; ks < kE / 4; ++ks) {
+        const int e = ks * 4 + fk;
+#pragma unroll
+        for (int i = 0; i < MTE; ++i) {
+            af[ks][i] = e < nr ? cs[e * CP + 8 * i] : 0.0;
+            const unsigned long long w = (unsigned long long)__double_as_longlong(af[ks][i]);
+            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            bf[ks][j] = e < nr ? rs[e * RP + 8 * j] : 0.0;
+            const unsigned long long w = (unsigned long long)__double_as_longlong(bf[ks][j]);
+            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
+        }
+    }
+    xr = __reduce_xor_sync(0xffffffffu, xr);
+    if (lane == 0) mbar_arrive_after(empty_s, (double)xr, sink_w);
+#pragma unroll
+    for (int ks = 0; ks < kE / 4; ++ks)
+#pragma unroll
+        for (int i = 0; i < MTE; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
+}
+
+// One CTA per tile walks every item in table order through one TMA ring (the
+// ring of fg_block_tma_kernel with staged coefficient rows; the pipeline does
+// not drain between items): an item's slices are t_first + j*stride, DMMA M
+// tiles beyond its steps are skipped, and its partial sums are flushed from the
+// accumulators when its last stage is done.
+template <int BT, int TP>
+__global__ void __launch_bounds__(TP + 32, 2)
+    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T, double* __restrict__ Q) {
+    constexpr int kStages = ring_stages<true>();
+    constexpr int RP = row_pitch<TP>();
+    constexpr int CP = coef_pitch<BT>();
+    constexpr int MT = BT / 8;
+    constexpr int NT = 4;
+    constexpr int NW = TP / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* rows = reinterpret_cast<double*>(smem);                        // [kStages][kE][RP]
+    double* coef = rows + kStages * kE * RP;                              // [kStages*kE][CP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kE * CP);
+    uint64_t* empty = full + kStages;
+    double* sink = reinterpret_cast<double*>(empty + kStages);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int64_t q0 = (int64_t)blockIdx.x * TP;  // single member: tile = point range
+    const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+    const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NW) {  // producer
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int64_t g = 0;  // stage counter over all items
+            for (int x = 0; x < T.n_items; ++x) {
+                const BlockItem& it = T.it[x];
+                const double* src0 = a.H + q0 + it.t_first * a.slice_stride;
+                const int64_t sstride = (int64_t)it.stride * a.slice_stride;
+                const double* c0 = a.gcoef + (int64_t)it.coef_row * CP;
+                for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+                    const int s = (int)(g % kStages);
+                    if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
+                    const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
+                    const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
+                    mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
+                    for (int e = 0; e < nr; ++e)
+                        bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (j0 + e) * sstride, row_bytes,
+                                      &full[s], pol);
+                    bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, cbytes, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+
+    const int fr = lane >> 2, fk = lane & 3;
+    double d[MT][NT][2];
+    int64_t g = 0;
+    for (int x = 0; x < T.n_items; ++x) {
+        const BlockItem& it = T.it[x];
+        const int mt = (it.ncols + 7) >> 3;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+        for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+            const int s = (int)(g % kStages);
+            mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
+            const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
+            const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
+            const double* cs = coef + (size_t)s * kE * CP + fr;
+            // warp-uniform branch per item: only the item's M tiles are issued
+            // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
+            switch (mt) {
+                case 1: item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
+                case 2: item_stage<2 <= MT ? 2 : MT, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
+                case 3: item_stage<3 <= MT ? 3 : MT, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
+                default: item_stage<MT, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
+            }
+        }
+        // flush this item's partial sums: row r = step col2step[r]
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int r = 8 * i + fr;
+            if (i >= mt || r >= it.ncols) continue;
+            double* out = T.direct ? a.P + (int64_t)it.col2step[r] * a.slice_stride
+                                   : Q + ((int64_t)it.q_row + r) * a.slice_stride;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
+                if (q >= a.n_m) continue;
+                double* o = out + q;
+                if (T.direct && T.accumulate) {
+                    const double2 old = ld_cg2(o);
+                    st_pair(o, __dadd_rn(old.x, d[i][j][0]), __dadd_rn(old.y, d[i][j][1]));
+                } else {
+                    st_pair(o, d[i][j][0], d[i][j][1]);
+                }
+            }
+        }
+    }
+}
+
+// P[b] = Σ of step b's item rows of Q, in the table's fixed order.
+__global__ void fg_item_reduce_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
+                                      const double* __restrict__ Q) {
+    const int b = blockIdx.y;
+    const int64_t pairs = (a.n_m + 1) / 2;
+    const int n = T.nq[b];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int r = 0; r < n; ++r) {
+            const double2 v = ld_cg2(Q + (int64_t)T.q[b][r] * a.slice_stride + 2 * i);
+            if (r == 0) {
+                acc = v;
+            } else {
+                acc.x = __dadd_rn(acc.x, v.x);
+                acc.y = __dadd_rn(acc.y, v.y);
+            }
+        }
+        st_pair(a.P + (int64_t)b * a.slice_stride + 2 * i, acc.x, acc.y);
+    }
+}
+
+template <int BT, int TP>
+size_t item_block_smem() {
+    constexpr int NS = ring_stages<true>();
+    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * coef_pitch<BT>() * sizeof(double) +
+           (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
 }
 
 // ------------------------------------------------------------------ ψ tables ---
@@ -1018,9 +1260,10 @@ double* block_P(const fg_plan* p, int64_t kb0) {
 // Coefficient rows of block kb0 (single member): buffer (kb0 / tblock) & 1 of
 // blkcoef_dev, h_slices rows of kCoefRow doubles each, so the next block's main
 // launch can rebuild its rows while this block's tail launch still reads these.
-constexpr int kCoefRow = 36;  // >= coef_pitch<kMaxTBlock>()
+int64_t coef_capacity(const fg_plan* p) { return (p->coef_rows > 0 ? p->coef_rows : p->h_slices) * kCoefRow; }
+
 double* block_coef(const fg_plan* p, int64_t kb0) {
-    return p->blkcoef_dev + ((kb0 / p->tblock) & 1) * p->h_slices * kCoefRow;
+    return p->blkcoef_dev + ((kb0 / p->tblock) & 1) * coef_capacity(p);
 }
 
 // Recent-weight rows of a temporal block: a.rw[k-kb0][m] = weight of offset m in
@@ -1119,6 +1362,7 @@ BlockVariant choose_block_variant(const fg_plan* p) {
     int64_t best_cost = INT64_MAX;
     for (int tp : cands) {
         if (force && atoi(force) != tp) continue;
+        if (p->tblock == 32 && tp == 256 && !force) continue;  // spills at 32 x 256
         const int64_t tiles = ((p->n_m + tp - 1) / tp) * p->B;
         const int64_t cost = ((tiles + sm_count() - 1) / sm_count()) * tp;
         if (cost < best_cost) {
@@ -1155,10 +1399,142 @@ BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& 
     return a;
 }
 
-// main launch: P = Σ over slices t < kb0 - tblock (all but the previous block's),
-// after the block's coefficient rows (single member).  Everything it reads is
-// final once step kb0 - tblock - 1 ... kb0 - 1's predecessor block is done, so
-// fg_run issues it on a side stream while the previous block's steps run.
+// Item table of block (kb0, bt) over slices [ts, te) (single member; see
+// fg_block_item_kernel).  Returns false when it does not fit the table or the
+// scratch buffers, and the caller uses the dense kernel.
+bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, ItemTable& T, int64_t row0) {
+    memset(&T, 0, sizeof T);
+    if (te <= ts) return true;  // no old slices: n_items = 0
+    const int64_t hz = p->kind == 1 ? p->horizon_max : 0;
+    FgSeg segs[FG_MAX_SEGS];
+    int64_t res[kMaxItems], tmin[kMaxItems], tmax[kMaxItems];
+    int n = 0;
+    for (int b = 0; b < bt; ++b) {
+        const int64_t k = kb0 + b;
+        const int ns = fg_segments(p->kind, k, p->base, hz, segs);
+        if (ns < 0 || ns > kBlkSegs) return false;  // the coefficient kernel keeps kBlkSegs
+        for (int si = 0; si < ns; ++si) {
+            const int64_t m0 = segs[si].m0, st = segs[si].stride, cnt = segs[si].count;
+            const int64_t m_min = k - te + 1, m_max = k - ts;  // t = k - m in [ts, te)
+            if (m_max < m0 || m_min > m0 + (cnt - 1) * st) continue;
+            const int64_t i0 = m_min > m0 ? (m_min - m0 + st - 1) / st : 0;
+            const int64_t i1 = (m_max - m0) / st < cnt - 1 ? (m_max - m0) / st : cnt - 1;
+            if (i0 > i1) continue;
+            const int64_t t_hi = k - (m0 + i0 * st), t_lo = k - (m0 + i1 * st);
+            const int64_t r = t_lo % st;
+            int x = -1;
+            for (int q = 0; q < n; ++q)
+                if (T.it[q].stride == st && res[q] == r) {
+                    x = q;
+                    break;
+                }
+            if (x < 0) {
+                if (n == kMaxItems) return false;
+                x = n++;
+                T.it[x].stride = (int32_t)st;
+                res[x] = r;
+                tmin[x] = t_lo;
+                tmax[x] = t_hi;
+            } else {
+                tmin[x] = t_lo < tmin[x] ? t_lo : tmin[x];
+                tmax[x] = t_hi > tmax[x] ? t_hi : tmax[x];
+            }
+            BlockItem& it = T.it[x];
+            if (it.ncols == 0 || it.col2step[it.ncols - 1] != b) it.col2step[it.ncols++] = (uint8_t)b;
+        }
+    }
+    T.n_items = n;
+    int64_t crow = row0, qrow = 0;
+    for (int x = 0; x < n; ++x) {
+        BlockItem& it = T.it[x];
+        it.t_first = tmin[x];
+        it.n_slices = (int32_t)((tmax[x] - tmin[x]) / it.stride + 1);
+        it.coef_row = (int32_t)crow;
+        crow += it.n_slices;
+        it.q_row = (int32_t)qrow;
+        qrow += it.ncols;
+    }
+    T.direct = n == 1 && T.it[0].ncols == bt;  // columns are appended in step order
+    for (int b = 0; b < bt && !T.direct; ++b) {
+        for (int x = 0; x < n; ++x) {
+            const BlockItem& it = T.it[x];
+            for (int c = 0; c < it.ncols; ++c)
+                if (it.col2step[c] == b) {
+                    if (T.nq[b] == kMaxQ) return false;
+                    T.q[b][T.nq[b]++] = (int16_t)(it.q_row + c);
+                }
+        }
+    }
+    const int64_t cp = p->tblock + 4;
+    if (crow * cp > coef_capacity(p)) return false;
+    if (!T.direct && (!p->Q_dev || qrow > p->q_rows)) return false;
+    return true;
+}
+
+template <int BT>
+int launch_items_bt(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st) {
+    double* rows = const_cast<double*>(a.gcoef);
+    int max_rows = 0;
+    for (int x = 0; x < T.n_items; ++x) max_rows = T.it[x].n_slices > max_rows ? T.it[x].n_slices : max_rows;
+    const unsigned cx = (unsigned)((max_rows * coef_pitch<BT>() + 255) / 256 < 16 ? (max_rows * coef_pitch<BT>() + 255) / 256 : 16);
+    fg_item_coef_kernel<BT><<<dim3(cx, (unsigned)T.n_items), 256, 0, st>>>(a, T, rows);
+    if (int rc = cuda_check(cudaGetLastError(), "fg_item_coef launch")) return rc;
+    void (*kern)(const BlockArgs, const ItemTable, double*) = nullptr;
+    size_t smem = 0;
+    switch (tp) {
+        case 128: kern = fg_block_item_kernel<BT, 128>; smem = item_block_smem<BT, 128>(); break;
+        case 192: kern = fg_block_item_kernel<BT, 192>; smem = item_block_smem<BT, 192>(); break;
+        case 224: kern = fg_block_item_kernel<BT, 224>; smem = item_block_smem<BT, 224>(); break;
+        default: kern = fg_block_item_kernel<BT, 256>; smem = item_block_smem<BT, 256>(); tp = 256; break;
+    }
+    if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                            "item smem attribute"))
+        return rc;
+    if (int rc = prefer_max_smem((const void*)kern)) return rc;
+    const unsigned tiles = (unsigned)((p->n_m + tp - 1) / tp);
+    kern<<<tiles, tp + 32, smem, st>>>(a, T, p->Q_dev);
+    if (int rc = cuda_check(cudaGetLastError(), "fg_block_item launch")) return rc;
+    if (!T.direct) {
+        const int64_t pairs = (p->n_m + 1) / 2;
+        const unsigned gx = (unsigned)((pairs + 255) / 256 < 256 ? (pairs + 255) / 256 : 256);
+        fg_item_reduce_kernel<<<dim3(gx, (unsigned)a.bt), 256, 0, st>>>(a, T, p->Q_dev);
+        if (int rc = cuda_check(cudaGetLastError(), "fg_item_reduce launch")) return rc;
+    }
+    return FG_OK;
+}
+
+// Dense coefficient rows (fg_block_coef_kernel) of slices [a.t_begin, a.t_end)
+// at a.gcoef, zeroed first.
+int launch_dense_coef(const fg_plan* p, const BlockArgs& a, cudaStream_t st) {
+    const int64_t hz = p->kind == 1 ? p->horizon_max : 0;
+    const int64_t t_lo = (p->kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
+    const int64_t ts = a.t_begin > t_lo ? a.t_begin : t_lo;
+    if (a.t_end <= ts) return FG_OK;
+    const size_t cp = (size_t)p->tblock + 4;  // coef_pitch<tblock>()
+    double* rows = const_cast<double*>(a.gcoef);
+    if (int rc = cuda_check(cudaMemsetAsync(rows, 0, (size_t)(a.t_end - ts) * cp * sizeof(double), st),
+                            "coefficient rows reset"))
+        return rc;
+    switch (p->tblock) {
+        case 8: fg_block_coef_kernel<8><<<a.bt, 256, 0, st>>>(a, rows); break;
+        case 24: fg_block_coef_kernel<24><<<a.bt, 256, 0, st>>>(a, rows); break;
+        case 32: fg_block_coef_kernel<32><<<a.bt, 256, 0, st>>>(a, rows); break;
+        default: fg_block_coef_kernel<16><<<a.bt, 256, 0, st>>>(a, rows); break;
+    }
+    return cuda_check(cudaGetLastError(), "fg_block_coef launch");
+}
+
+// FGB200_BLOCK_ITEMS=0 forces the dense main launch (same results within rounding).
+bool items_enabled() {
+    const char* e = getenv("FGB200_BLOCK_ITEMS");
+    return !(e && e[0] == '0');
+}
+
+// main launch: P = Σ over slices t < kb0 - tblock (all but the previous block's).
+// Everything it reads is final once the previous block starts, so fg_run
+// issues it on a side stream while the previous block's steps run.  Single
+// member: coefficient buffer = [tail rows (tblock)][main rows]; the tail rows
+// are built here too so the tail launch (on the critical path) only multiplies.
 int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (kb0 <= 0) {  // nothing older than the block: P = 0
         return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
@@ -1169,26 +1545,31 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     BlockArgs a = block_args(p, kb0, bt, v);
     a.t_begin = 0;
     a.t_end = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
+    if (a.gcoef) {
+        const int64_t cp = p->tblock + 4;
+        BlockArgs tail = a;  // tail rows at the buffer start
+        tail.t_begin = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
+        tail.t_end = kb0;
+        if (int rc = launch_dense_coef(p, tail, st)) return rc;
+        a.gcoef += p->tblock * cp;
+        ItemTable T;
+        if (items_enabled() && build_items(p, kb0, bt, 0, a.t_end, T, 0)) {
+            if (T.n_items == 0)
+                return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->ms * sizeof(double), st),
+                                  "P reset");
+            switch (p->tblock) {
+                case 8: return launch_items_bt<8>(p, a, T, v.tp, st);
+                case 24: return launch_items_bt<24>(p, a, T, v.tp, st);
+                case 32: return launch_items_bt<32>(p, a, T, v.tp, st);
+                default: return launch_items_bt<16>(p, a, T, v.tp, st);
+            }
+        }
+        if (int rc = launch_dense_coef(p, a, st)) return rc;
+    }
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
-    if (a.gcoef) {  // coefficient rows computed once for all tiles (main and tail)
-        const int64_t hz_host = p->kind == 1 ? p->horizon_max : 0;  // B == 1: the member's horizon
-        const int64_t t_lo = (p->kind == 1 && kb0 - hz_host > 0) ? kb0 - hz_host : 0;
-        const size_t cp = (size_t)p->tblock + 4;  // coef_pitch<tblock>()
-        if (int rc = cuda_check(cudaMemsetAsync(const_cast<double*>(a.gcoef), 0, (size_t)(kb0 - t_lo) * cp * sizeof(double), st),
-                                "coefficient rows reset"))
-            return rc;
-        double* rows = const_cast<double*>(a.gcoef);
-        switch (p->tblock) {
-            case 8: fg_block_coef_kernel<8><<<bt, 256, 0, st>>>(a, rows); break;
-            case 24: fg_block_coef_kernel<24><<<bt, 256, 0, st>>>(a, rows); break;
-            case 32: fg_block_coef_kernel<32><<<bt, 256, 0, st>>>(a, rows); break;
-            default: fg_block_coef_kernel<16><<<bt, 256, 0, st>>>(a, rows); break;
-        }
-        if (int rc = cuda_check(cudaGetLastError(), "fg_block_coef launch")) return rc;
-    }
     v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
@@ -1203,6 +1584,9 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     a.t_begin = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
     a.t_end = kb0;
     a.accumulate = 1;
+    if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
+                            "block smem attribute"))
+        return rc;
     v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
