@@ -207,11 +207,16 @@ __device__ __forceinline__ int64_t entries_upto(const FgSeg* s, int n, int64_t m
 }
 
 
-template <int NDIM, int REACT, int S>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __grid_constant__ StepArgs a) {
-    constexpr int kCols = (kThreads / 32) / S;   // warps across a tile
-    constexpr int TP = kCols * 32 * kVec;        // points per tile
-    constexpr int kLanes = kCols * 32;           // split-0 threads (one point pair each)
+// General A phase (unblocked steps): schedule of step k in shared memory, every
+// entry with m >= 2 streamed into s_acc; also returns the schedule length and
+// the weight of m = 1 for phase C.  Its shared staging exists only in the
+// kernels that call it (not in the temporal-blocking variant).
+template <int S>
+__device__ __forceinline__ void general_a_phase(const StepArgs& a, int64_t k, double2* s_acc, int64_t& len,
+                                                int64_t& w1, bool& has_m1) {
+    constexpr int kCols = (kThreads / 32) / S;
+    constexpr int TP = kCols * 32 * kVec;
+    constexpr int kLanes = kCols * 32;
     __shared__ FgSeg segs[FG_MAX_SEGS];
     __shared__ int64_t seg_first[FG_MAX_SEGS + 1];
     __shared__ int s_nseg;
@@ -220,6 +225,120 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
     __shared__ int32_t s_w[kChunk];
     __shared__ double s_c[kChunk];
     __shared__ double2 s_part[S > 1 ? (S - 1) * kLanes : 1];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int col = warp % kCols, split = warp / kCols;
+    const int slot = col * 32 + lane;
+    const int G = gridDim.x;
+    const int64_t bb = k - a.kb0;
+    // ================= A: schedule + old slices (m >= 2) =================
+    for (int i = tid; i < a.passes * kLanes; i += kThreads) s_acc[i] = make_double2(0.0, 0.0);
+    if (tid == 0) {
+        int n = fg_segments(a.kind, k, a.base, a.hz_max, segs);
+        int64_t acc = 0;
+        for (int i = 0; i < n; ++i) {
+            seg_first[i] = acc;
+            acc += segs[i].count;
+        }
+        seg_first[n] = acc;
+        s_nseg = n;
+        // temporal blocking: entries with m > bb (slices t < kb0) are already
+        // summed into P by fg_block_kernel; only m <= bb remain for this step
+        s_lim = a.blocked ? entries_upto(segs, n, k - a.kb0) : acc;
+    }
+    __syncthreads();
+    const int nseg = s_nseg;
+    len = seg_first[nseg];
+    const int64_t lim = s_lim;
+    // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
+    // m = 1 whenever the schedule has it.  Both depend on step k-1's output
+    // and are summed in phase C; entries from 2 on read slices t <= k-2.
+    const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
+    w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
+    has_m1 = len >= 2 && m1 == 1 && (!a.blocked || bb >= 1);
+    const int64_t old = (len >= 2 && m1 == 1) ? 2 : 1;
+
+    for (int64_t c0 = old; c0 < lim; c0 += kChunk) {
+        const int cn = (int)((lim - c0) < kChunk ? (lim - c0) : kChunk);
+        for (int e = tid; e < cn; e += kThreads) {
+            const int64_t j = c0 + e;
+            int si = 0;
+            while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
+            const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
+            s_t[e] = (int32_t)(k - m);
+            s_w[e] = (int32_t)segs[si].stride;
+        }
+        int64_t cur_member = -1;
+        for (int p = 0; p < a.passes; ++p) {
+            const int tile = blockIdx.x + p * G;
+            if (tile >= a.total_tiles) break;
+            const int64_t b = tile / a.tpm;
+            if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
+                __syncthreads();
+                const double* psi_b = a.psi + b * a.psi_stride;
+                for (int e = tid; e < cn; e += kThreads)
+                    s_c[e] = __dmul_rn((double)s_w[e], __ldg(psi_b + (k - s_t[e])));
+                __syncthreads();
+                cur_member = b;
+            }
+            int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+            if (len_b > lim) len_b = lim;
+            const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
+            const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
+            double acc0 = 0.0, acc1 = 0.0;
+            if (q < a.n_m) {
+                const double* hbase = a.H + b * a.ms + q;
+                for (int e0 = split; e0 < cnb; e0 += S * kUnroll) {
+                    double2 v[kUnroll];
+                    double c[kUnroll];
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        const int e = e0 + u * S;
+                        if (e < cnb) {
+                            v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
+                            c[u] = s_c[e];
+                        } else {
+                            v[u] = make_double2(0.0, 0.0);
+                            c[u] = 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        acc0 = fma(c[u], v[u].x, acc0);
+                        acc1 = fma(c[u], v[u].y, acc1);
+                    }
+                }
+            }
+            if (S > 1) {
+                if (split > 0) s_part[(split - 1) * kLanes + slot] = make_double2(acc0, acc1);
+                __syncthreads();
+                if (split == 0) {
+#pragma unroll
+                    for (int s = 1; s < S; ++s) {
+                        const double2 pp = s_part[(s - 1) * kLanes + slot];
+                        acc0 = __dadd_rn(acc0, pp.x);
+                        acc1 = __dadd_rn(acc1, pp.y);
+                    }
+                }
+                __syncthreads();
+            }
+            if (split == 0) {
+                double2& r = s_acc[p * kLanes + slot];
+                r.x = __dadd_rn(r.x, acc0);
+                r.y = __dadd_rn(r.y, acc1);
+            }
+        }
+        __syncthreads();  // s_t / s_w / s_c are refilled by the next chunk
+    }
+}
+
+// BLK: temporal-blocking variant (S = 1): the recent-slice A phase only, no
+// shared staging, so two of its CTAs fit next to two block-kernel CTAs per SM.
+template <int NDIM, int REACT, int S, bool BLK>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __grid_constant__ StepArgs a) {
+    constexpr int kCols = (kThreads / 32) / S;   // warps across a tile
+    constexpr int TP = kCols * 32 * kVec;        // points per tile
+    constexpr int kLanes = kCols * 32;           // split-0 threads (one point pair each)
     extern __shared__ double2 s_acc[];  // [passes][kLanes] partial sums of the A phase
 
     const int tid = threadIdx.x;
@@ -233,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
         const int64_t bb = k - a.kb0;
         int64_t len, w1;   // schedule length (kinds 0/2), weight of m = 1
         bool has_m1;
-        if (S == 1 && a.blocked) {
+        if constexpr (BLK) {
             w1 = bb >= 1 ? a.rw[bb][1] : 0;
             has_m1 = w1 != 0;
             len = k + 1;  // only used for the m = 1 test below (k >= bb >= 1)
@@ -279,106 +398,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 s_acc[p * kLanes + slot] = make_double2(__dadd_rn(0.0, acc0), __dadd_rn(0.0, acc1));
             }
         } else {
-            // ================= A: schedule + old slices (m >= 2) =================
-            for (int i = tid; i < a.passes * kLanes; i += kThreads) s_acc[i] = make_double2(0.0, 0.0);
-            if (tid == 0) {
-                int n = fg_segments(a.kind, k, a.base, a.hz_max, segs);
-                int64_t acc = 0;
-                for (int i = 0; i < n; ++i) {
-                    seg_first[i] = acc;
-                    acc += segs[i].count;
-                }
-                seg_first[n] = acc;
-                s_nseg = n;
-                // temporal blocking: entries with m > bb (slices t < kb0) are already
-                // summed into P by fg_block_kernel; only m <= bb remain for this step
-                s_lim = a.blocked ? entries_upto(segs, n, k - a.kb0) : acc;
-            }
-            __syncthreads();
-            const int nseg = s_nseg;
-            len = seg_first[nseg];
-            const int64_t lim = s_lim;
-            // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
-            // m = 1 whenever the schedule has it.  Both depend on step k-1's output
-            // and are summed in phase C; entries from 2 on read slices t <= k-2.
-            const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
-            w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
-            has_m1 = len >= 2 && m1 == 1 && (!a.blocked || bb >= 1);
-            const int64_t old = (len >= 2 && m1 == 1) ? 2 : 1;
-
-            for (int64_t c0 = old; c0 < lim; c0 += kChunk) {
-                const int cn = (int)((lim - c0) < kChunk ? (lim - c0) : kChunk);
-                for (int e = tid; e < cn; e += kThreads) {
-                    const int64_t j = c0 + e;
-                    int si = 0;
-                    while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
-                    const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
-                    s_t[e] = (int32_t)(k - m);
-                    s_w[e] = (int32_t)segs[si].stride;
-                }
-                int64_t cur_member = -1;
-                for (int p = 0; p < a.passes; ++p) {
-                    const int tile = blockIdx.x + p * G;
-                    if (tile >= a.total_tiles) break;
-                    const int64_t b = tile / a.tpm;
-                    if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
-                        __syncthreads();
-                        const double* psi_b = a.psi + b * a.psi_stride;
-                        for (int e = tid; e < cn; e += kThreads)
-                            s_c[e] = __dmul_rn((double)s_w[e], __ldg(psi_b + (k - s_t[e])));
-                        __syncthreads();
-                        cur_member = b;
-                    }
-                    int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
-                    if (len_b > lim) len_b = lim;
-                    const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
-                    const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
-                    double acc0 = 0.0, acc1 = 0.0;
-                    if (q < a.n_m) {
-                        const double* hbase = a.H + b * a.ms + q;
-                        for (int e0 = split; e0 < cnb; e0 += S * kUnroll) {
-                            double2 v[kUnroll];
-                            double c[kUnroll];
-#pragma unroll
-                            for (int u = 0; u < kUnroll; ++u) {
-                                const int e = e0 + u * S;
-                                if (e < cnb) {
-                                    v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
-                                    c[u] = s_c[e];
-                                } else {
-                                    v[u] = make_double2(0.0, 0.0);
-                                    c[u] = 0.0;
-                                }
-                            }
-#pragma unroll
-                            for (int u = 0; u < kUnroll; ++u) {
-                                acc0 = fma(c[u], v[u].x, acc0);
-                                acc1 = fma(c[u], v[u].y, acc1);
-                            }
-                        }
-                    }
-                    if (S > 1) {
-                        if (split > 0) s_part[(split - 1) * kLanes + slot] = make_double2(acc0, acc1);
-                        __syncthreads();
-                        if (split == 0) {
-#pragma unroll
-                            for (int s = 1; s < S; ++s) {
-                                const double2 pp = s_part[(s - 1) * kLanes + slot];
-                                acc0 = __dadd_rn(acc0, pp.x);
-                                acc1 = __dadd_rn(acc1, pp.y);
-                            }
-                        }
-                        __syncthreads();
-                    }
-                    if (split == 0) {
-                        double2& r = s_acc[p * kLanes + slot];
-                        r.x = __dadd_rn(r.x, acc0);
-                        r.y = __dadd_rn(r.y, acc1);
-                    }
-                }
-                __syncthreads();  // s_t / s_w / s_c are refilled by the next chunk
-            }
-        }  // general A phase
+            general_a_phase<S>(a, k, s_acc, len, w1, has_m1);
+        }
 
         // ================= dependency on step k-1 =================
         if (multi) {
@@ -665,11 +686,10 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
-    const int64_t mem = tile / a.tpm;
-    const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
-    const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
-    const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+    // Tiles blockIdx.x, +gridDim.x, ...: single-member launches run one CTA per
+    // SM over several tiles (room for the concurrent step kernel); ensembles
+    // launch one CTA per tile, so every tile of a CTA has the same member.
+    const int64_t mem = blockIdx.x / a.tpm;
     const int64_t hz = a.kind == 1 ? a.horizon[mem] : 0;
     // oldest slice any step of the block can reach: short memory stops at kb0 - H
     const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
@@ -693,19 +713,25 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 
     if (warp == NW) {  // ---- producer: lane 0 drives the bulk-copy ring
         if (lane == 0) {
-            const double* src0 = a.H + mem * a.ms + q0;
             const uint64_t pol = l2_evict_first_policy();
-            for (int64_t g = 0; g < n_st; ++g) {
-                const int s = (int)(g % kStages);
-                if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                const int64_t t0 = ts + g * kE;
-                const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
-                const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
-                mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
-                for (int e = 0; e < nr; ++e)
-                    bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
-                                  &full[s], pol);
-                if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
+            int64_t g = 0;  // stage counter over all tiles of the CTA
+            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+                const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
+                const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+                const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+                const double* src0 = a.H + mem * a.ms + q0;
+                for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
+                    const int s = (int)(g % kStages);
+                    if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
+                    const int64_t t0 = ts + gl * kE;
+                    const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
+                    const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
+                    mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
+                    for (int e = 0; e < nr; ++e)
+                        bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
+                                      &full[s], pol);
+                    if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
+                }
             }
         }
         return;
@@ -714,15 +740,18 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     // ---- consumers: warp w owns points [32w, 32w+32) of the tile
     const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
     const double* psi_b = a.psi + mem * a.psi_stride;
+    const int ngroups = TP / BT;  // threads per step column when filling the table
+    int64_t g = 0;
+    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
     double d[MT][NT][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
-    const int ngroups = TP / BT;  // threads per step column when filling the table
-    for (int64_t g = 0; g < n_st; ++g) {
-        const int64_t t0 = ts + g * kE;
-        if (!staged && (g * kE) % kCH == 0) {
+    for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
+        const int64_t t0 = ts + gl * kE;
+        if (!staged && (gl * kE) % kCH == 0) {
             // ensemble path: coefficient table for slices t0 .. t0+kCH-1 — zero it,
             // then scatter w·ψ_b(m) over every schedule segment (no per-slice search)
             asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
@@ -751,7 +780,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
         const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
         const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
-        const double* cs = (staged ? coef + (size_t)s * kE * CP : coef + ((g * kE) % kCH) * CP) + fr;
+        const double* cs = (staged ? coef + (size_t)s * kE * CP : coef + ((gl * kE) % kCH) * CP) + fr;
         // all fragments of the stage into registers first ...
         double af[kE / 4][MT], bf[kE / 4][NT];
         uint32_t x = 0;
@@ -803,6 +832,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
             }
         }
     }
+    }  // tiles
 }
 
 // ------------------------------------------- class-decomposed block stage ---
@@ -819,16 +849,19 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 // Q; a fixed-order reduction sums each step's rows into P (deterministic).
 // Full and short memory are one item (s = 1, every step) written to P directly.
 
-constexpr int kMaxItems = 112;
-constexpr int kMaxQ = 8;  // items a step may appear in (distinct strides)
+constexpr int kMaxItems = 160;
+constexpr int kMaxQ = 8;        // items a step may appear in (distinct strides)
+constexpr int kItemCols = 8;    // steps per item: one DMMA M tile, so the kernel's
+                                // accumulators (and registers) do not grow with tblock
+constexpr int kItemPitch = kItemCols + 4;  // coefficient row pitch (conflict-free, see coef_pitch)
 
 struct BlockItem {
     int64_t t_first;
     int32_t stride, n_slices;
     int32_t coef_row;  // first coefficient row (kCoefRow doubles each) of this item
     int32_t q_row;     // first Q row (direct mode: unused)
-    int32_t ncols;     // steps in the item; column c is step col2step[c]
-    uint8_t col2step[kMaxTBlock];
+    int32_t ncols;     // steps in the item (<= kItemCols); column c is step col2step[c]
+    uint8_t col2step[kItemCols];
 };
 
 struct ItemTable {
@@ -845,12 +878,11 @@ struct ItemTable {
 // w·ψ(kb0 + col2step[c] - t_j) when that offset is in step col2step[c]'s
 // schedule with weight w == the item's stride (the entry belongs to this
 // item), else 0; columns ncols..CP-1 are zero padding for the DMMA tiles.
-template <int BT>
 __global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
                                     double* __restrict__ out) {
-    constexpr int CP = coef_pitch<BT>();
-    __shared__ FgSeg segs[BT][kBlkSegs];
-    __shared__ int nseg[BT];
+    constexpr int CP = kItemPitch;
+    __shared__ FgSeg segs[kItemCols][kBlkSegs];
+    __shared__ int nseg[kItemCols];
     const BlockItem& it = T.it[blockIdx.y];
     const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
     if (threadIdx.x < it.ncols) {
@@ -913,13 +945,13 @@ __device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double*
 // not drain between items): an item's slices are t_first + j*stride, DMMA M
 // tiles beyond its steps are skipped, and its partial sums are flushed from the
 // accumulators when its last stage is done.
-template <int BT, int TP>
-__global__ void __launch_bounds__(TP + 32, 2)
+template <int TP>
+__global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leave room for two step CTAs
     fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T, double* __restrict__ Q) {
     constexpr int kStages = ring_stages<true>();
     constexpr int RP = row_pitch<TP>();
-    constexpr int CP = coef_pitch<BT>();
-    constexpr int MT = BT / 8;
+    constexpr int CP = kItemPitch;
+    constexpr int MT = 1;
     constexpr int NT = 4;
     constexpr int NW = TP / 32;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -931,9 +963,6 @@ __global__ void __launch_bounds__(TP + 32, 2)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int64_t q0 = (int64_t)blockIdx.x * TP;  // single member: tile = point range
-    const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
-    const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -947,8 +976,12 @@ __global__ void __launch_bounds__(TP + 32, 2)
     if (warp == NW) {  // producer
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
-            int64_t g = 0;  // stage counter over all items
-            for (int x = 0; x < T.n_items; ++x) {
+            int64_t g = 0;  // stage counter over all tiles and items
+            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            const int64_t q0 = (int64_t)tile * TP;  // single member: tile = point range
+            const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+            const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+            for (int x = blockIdx.y; x < T.n_items; x += gridDim.y) {
                 const BlockItem& it = T.it[x];
                 const double* src0 = a.H + q0 + it.t_first * a.slice_stride;
                 const int64_t sstride = (int64_t)it.stride * a.slice_stride;
@@ -965,6 +998,7 @@ __global__ void __launch_bounds__(TP + 32, 2)
                     bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, cbytes, &full[s]);
                 }
             }
+            }  // tiles
         }
         return;
     }
@@ -972,7 +1006,9 @@ __global__ void __launch_bounds__(TP + 32, 2)
     const int fr = lane >> 2, fk = lane & 3;
     double d[MT][NT][2];
     int64_t g = 0;
-    for (int x = 0; x < T.n_items; ++x) {
+    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    const int64_t q0 = (int64_t)tile * TP;
+    for (int x = blockIdx.y; x < T.n_items; x += gridDim.y) {
         const BlockItem& it = T.it[x];
         const int mt = (it.ncols + 7) >> 3;
 #pragma unroll
@@ -987,12 +1023,7 @@ __global__ void __launch_bounds__(TP + 32, 2)
             const double* cs = coef + (size_t)s * kE * CP + fr;
             // warp-uniform branch per item: only the item's M tiles are issued
             // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
-            switch (mt) {
-                case 1: item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
-                case 2: item_stage<2 <= MT ? 2 : MT, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
-                case 3: item_stage<3 <= MT ? 3 : MT, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
-                default: item_stage<MT, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp); break;
-            }
+            item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
         }
         // flush this item's partial sums: row r = step col2step[r]
 #pragma unroll
@@ -1015,6 +1046,7 @@ __global__ void __launch_bounds__(TP + 32, 2)
             }
         }
     }
+    }  // tiles
 }
 
 // P[b] = Σ of step b's item rows of Q, in the table's fixed order.
@@ -1038,10 +1070,10 @@ __global__ void fg_item_reduce_kernel(const BlockArgs a, const __grid_constant__
     }
 }
 
-template <int BT, int TP>
+template <int TP>
 size_t item_block_smem() {
     constexpr int NS = ring_stages<true>();
-    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * coef_pitch<BT>() * sizeof(double) +
+    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * kItemPitch * sizeof(double) +
            (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
 }
 
@@ -1203,19 +1235,22 @@ int choose_split(const fg_plan* p) {
 typedef void (*StepKernel)(const StepArgs);
 
 template <int NDIM, int REACT>
-StepKernel pick_s(int s) {
+StepKernel pick_s(int s, bool blk) {
+    if (blk) return fg_step_kernel<NDIM, REACT, 1, true>;
     switch (s) {
-        case 1: return fg_step_kernel<NDIM, REACT, 1>;
-        case 2: return fg_step_kernel<NDIM, REACT, 2>;
-        case 4: return fg_step_kernel<NDIM, REACT, 4>;
-        default: return fg_step_kernel<NDIM, REACT, 8>;
+        case 1: return fg_step_kernel<NDIM, REACT, 1, false>;
+        case 2: return fg_step_kernel<NDIM, REACT, 2, false>;
+        case 4: return fg_step_kernel<NDIM, REACT, 4, false>;
+        default: return fg_step_kernel<NDIM, REACT, 8, false>;
     }
 }
 
-StepKernel pick_kernel(int ndim, int react, int s) {
-    if (ndim == 1) return react ? pick_s<1, 1>(s) : pick_s<1, 0>(s);
-    if (ndim == 2) return react ? pick_s<2, 1>(s) : pick_s<2, 0>(s);
-    return react ? pick_s<3, 1>(s) : pick_s<3, 0>(s);
+// blk: a temporal-blocking launch with no warp split (the recent-slice kernel)
+StepKernel pick_kernel(int ndim, int react, int s, bool blk = false) {
+    blk = blk && s == 1;
+    if (ndim == 1) return react ? pick_s<1, 1>(s, blk) : pick_s<1, 0>(s, blk);
+    if (ndim == 2) return react ? pick_s<2, 1>(s, blk) : pick_s<2, 0>(s, blk);
+    return react ? pick_s<3, 1>(s, blk) : pick_s<3, 0>(s, blk);
 }
 
 StepArgs make_args(const fg_plan* p, int s) {
@@ -1315,7 +1350,7 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
         a.P = block_P(p, kb0);
         fill_recent(a, p, kb0, k, k + 1);
     }
-    StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
+    StepKernel kern = pick_kernel(p->ndim, p->reaction, s, kb0 >= 0);
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.total_tiles, 1, 1);
@@ -1378,6 +1413,17 @@ BlockVariant choose_block_variant(const fg_plan* p) {
     return best;
 }
 
+// Block-kernel grid: ensembles one CTA per tile; single members at most
+// FGB200_BLOCK_CTAS_PER_SM (default 2) CTAs per SM looping over tiles (one wave;
+// 1 leaves room for the concurrent steps but halves the stream rate).
+unsigned block_grid(const fg_plan* p, int64_t total_tiles) {
+    if (p->B != 1) return (unsigned)total_tiles;
+    const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
+    const int per = e ? atoi(e) : 2;
+    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
+    return (unsigned)(total_tiles < cap ? total_tiles : cap);
+}
+
 BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& v) {
     BlockArgs a;
     memset(&a, 0, sizeof a);
@@ -1406,9 +1452,16 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
     memset(&T, 0, sizeof T);
     if (te <= ts) return true;  // no old slices: n_items = 0
     const int64_t hz = p->kind == 1 ? p->horizon_max : 0;
+    // groups: same stride and residue, slice ranges within a few strides of
+    // each other (a far-apart range of the same class starts a new group)
+    struct Grp {
+        int64_t s, r, tmin, tmax;
+        int n;
+        uint8_t cols[kMaxTBlock];
+    };
+    static thread_local Grp g[kMaxItems];
+    int ng = 0;
     FgSeg segs[FG_MAX_SEGS];
-    int64_t res[kMaxItems], tmin[kMaxItems], tmax[kMaxItems];
-    int n = 0;
     for (int b = 0; b < bt; ++b) {
         const int64_t k = kb0 + b;
         const int ns = fg_segments(p->kind, k, p->base, hz, segs);
@@ -1421,39 +1474,49 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
             const int64_t i1 = (m_max - m0) / st < cnt - 1 ? (m_max - m0) / st : cnt - 1;
             if (i0 > i1) continue;
             const int64_t t_hi = k - (m0 + i0 * st), t_lo = k - (m0 + i1 * st);
-            const int64_t r = t_lo % st;
+            const int64_t r = t_lo % st, gap = 8 * st;
             int x = -1;
-            for (int q = 0; q < n; ++q)
-                if (T.it[q].stride == st && res[q] == r) {
+            for (int q = 0; q < ng; ++q)
+                if (g[q].s == st && g[q].r == r && t_lo <= g[q].tmax + gap && t_hi >= g[q].tmin - gap) {
                     x = q;
                     break;
                 }
             if (x < 0) {
-                if (n == kMaxItems) return false;
-                x = n++;
-                T.it[x].stride = (int32_t)st;
-                res[x] = r;
-                tmin[x] = t_lo;
-                tmax[x] = t_hi;
+                if (ng == kMaxItems) return false;
+                x = ng++;
+                g[x].s = st;
+                g[x].r = r;
+                g[x].tmin = t_lo;
+                g[x].tmax = t_hi;
+                g[x].n = 0;
             } else {
-                tmin[x] = t_lo < tmin[x] ? t_lo : tmin[x];
-                tmax[x] = t_hi > tmax[x] ? t_hi : tmax[x];
+                g[x].tmin = t_lo < g[x].tmin ? t_lo : g[x].tmin;
+                g[x].tmax = t_hi > g[x].tmax ? t_hi : g[x].tmax;
             }
-            BlockItem& it = T.it[x];
-            if (it.ncols == 0 || it.col2step[it.ncols - 1] != b) it.col2step[it.ncols++] = (uint8_t)b;
+            if (g[x].n == 0 || g[x].cols[g[x].n - 1] != b) g[x].cols[g[x].n++] = (uint8_t)b;
+        }
+    }
+    // one dense class holding every step (full / short memory): the dense kernel
+    // streams it once for all steps; items would re-read it per 8 steps
+    if (ng == 1 && g[0].s == 1 && g[0].n == bt && bt > kItemCols) return false;
+    int n = 0;
+    int64_t crow = row0, qrow = 0;
+    for (int x = 0; x < ng; ++x) {
+        for (int c0 = 0; c0 < g[x].n; c0 += kItemCols) {
+            if (n == kMaxItems) return false;
+            BlockItem& it = T.it[n++];
+            it.t_first = g[x].tmin;
+            it.stride = (int32_t)g[x].s;
+            it.n_slices = (int32_t)((g[x].tmax - g[x].tmin) / g[x].s + 1);
+            it.ncols = g[x].n - c0 < kItemCols ? g[x].n - c0 : kItemCols;
+            for (int c = 0; c < it.ncols; ++c) it.col2step[c] = g[x].cols[c0 + c];
+            it.coef_row = (int32_t)crow;
+            crow += it.n_slices;
+            it.q_row = (int32_t)qrow;
+            qrow += it.ncols;
         }
     }
     T.n_items = n;
-    int64_t crow = row0, qrow = 0;
-    for (int x = 0; x < n; ++x) {
-        BlockItem& it = T.it[x];
-        it.t_first = tmin[x];
-        it.n_slices = (int32_t)((tmax[x] - tmin[x]) / it.stride + 1);
-        it.coef_row = (int32_t)crow;
-        crow += it.n_slices;
-        it.q_row = (int32_t)qrow;
-        qrow += it.ncols;
-    }
     T.direct = n == 1 && T.it[0].ncols == bt;  // columns are appended in step order
     for (int b = 0; b < bt && !T.direct; ++b) {
         for (int x = 0; x < n; ++x) {
@@ -1465,34 +1528,36 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
                 }
         }
     }
-    const int64_t cp = p->tblock + 4;
-    if (crow * cp > coef_capacity(p)) return false;
+    if (crow * kItemPitch > coef_capacity(p)) return false;
     if (!T.direct && (!p->Q_dev || qrow > p->q_rows)) return false;
     return true;
 }
 
-template <int BT>
-int launch_items_bt(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st) {
+int launch_items(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st) {
     double* rows = const_cast<double*>(a.gcoef);
     int max_rows = 0;
     for (int x = 0; x < T.n_items; ++x) max_rows = T.it[x].n_slices > max_rows ? T.it[x].n_slices : max_rows;
-    const unsigned cx = (unsigned)((max_rows * coef_pitch<BT>() + 255) / 256 < 16 ? (max_rows * coef_pitch<BT>() + 255) / 256 : 16);
-    fg_item_coef_kernel<BT><<<dim3(cx, (unsigned)T.n_items), 256, 0, st>>>(a, T, rows);
+    const int cx = (max_rows * kItemPitch + 255) / 256;
+    fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items), 256, 0, st>>>(a, T, rows);
     if (int rc = cuda_check(cudaGetLastError(), "fg_item_coef launch")) return rc;
     void (*kern)(const BlockArgs, const ItemTable, double*) = nullptr;
     size_t smem = 0;
     switch (tp) {
-        case 128: kern = fg_block_item_kernel<BT, 128>; smem = item_block_smem<BT, 128>(); break;
-        case 192: kern = fg_block_item_kernel<BT, 192>; smem = item_block_smem<BT, 192>(); break;
-        case 224: kern = fg_block_item_kernel<BT, 224>; smem = item_block_smem<BT, 224>(); break;
-        default: kern = fg_block_item_kernel<BT, 256>; smem = item_block_smem<BT, 256>(); tp = 256; break;
+        case 128: kern = fg_block_item_kernel<128>; smem = item_block_smem<128>(); break;
+        case 192: kern = fg_block_item_kernel<192>; smem = item_block_smem<192>(); break;
+        case 224: kern = fg_block_item_kernel<224>; smem = item_block_smem<224>(); break;
+        default: kern = fg_block_item_kernel<256>; smem = item_block_smem<256>(); tp = 256; break;
     }
     if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                             "item smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
-    const unsigned tiles = (unsigned)((p->n_m + tp - 1) / tp);
-    kern<<<tiles, tp + 32, smem, st>>>(a, T, p->Q_dev);
+    // FGB200_ITEM_GRID=1: one CTA per (tile, item); default: one CTA per tile
+    // (at most FGB200_BLOCK_CTAS_PER_SM per SM) walks all items
+    const char* ig = getenv("FGB200_ITEM_GRID");
+    const bool per_item = ig && ig[0] == '1';
+    const dim3 grid = per_item ? dim3((unsigned)a.total_tiles, (unsigned)T.n_items) : dim3(block_grid(p, a.total_tiles));
+    kern<<<grid, tp + 32, smem, st>>>(a, T, p->Q_dev);
     if (int rc = cuda_check(cudaGetLastError(), "fg_block_item launch")) return rc;
     if (!T.direct) {
         const int64_t pairs = (p->n_m + 1) / 2;
@@ -1557,12 +1622,7 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
             if (T.n_items == 0)
                 return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->ms * sizeof(double), st),
                                   "P reset");
-            switch (p->tblock) {
-                case 8: return launch_items_bt<8>(p, a, T, v.tp, st);
-                case 24: return launch_items_bt<24>(p, a, T, v.tp, st);
-                case 32: return launch_items_bt<32>(p, a, T, v.tp, st);
-                default: return launch_items_bt<16>(p, a, T, v.tp, st);
-            }
+            return launch_items(p, a, T, v.tp, st);
         }
         if (int rc = launch_dense_coef(p, a, st)) return rc;
     }
@@ -1570,7 +1630,7 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
                             "block smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
-    v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
+    v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
 
@@ -1587,7 +1647,7 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
         return rc;
-    v.kern<<<(unsigned)a.total_tiles, v.tp + 32, v.smem, st>>>(a);
+    v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
 
@@ -1682,7 +1742,7 @@ int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cu
         a.P = block_P(p, kb0);
         fill_recent(a, p, kb0, k0, k1);
     }
-    StepKernel kern = pick_kernel(p->ndim, p->reaction, s);
+    StepKernel kern = pick_kernel(p->ndim, p->reaction, s, kb0 >= 0);
     const size_t smem = acc_smem(s, passes);
     if (smem > 48 * 1024) {
         if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
