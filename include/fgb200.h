@@ -85,15 +85,15 @@ typedef struct fg_plan {
     int32_t* snap_slot_dev;      /* [h_slices+1] scratch for FG_RUN_PERSISTENT snapshots
                                     (filled by fg_run; NULL if no snapshots)       */
     int64_t horizon_max;         /* host copy of max(horizon_dev) (0 = unknown)    */
-    int32_t tblock;              /* temporal blocking factor: 0 (off), 8 or 16     */
+    int32_t tblock;              /* temporal blocking factor: 0 (off), 8, 16, 24, 32;
+                                    48 / 64 for single-member adaptive plans only  */
     int32_t reserved2;
     double* P_dev;               /* [2][tblock][B*ms] scratch for blocked partial sums:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
     double* blkcoef_dev;         /* [2][coef_rows][36] scratch, single-member blocking:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
-    double* Q_dev;               /* [q_rows][B*ms] scratch, single-member thinned
-                                    schedules: per-item partial sums (NULL: dense)  */
-    int64_t q_rows;
+    double* Q_dev;               /* reserved, NULL                                   */
+    int64_t q_rows;              /* reserved, 0                                      */
     int64_t coef_rows;           /* rows per blkcoef buffer (0 = h_slices)          */
 } fg_plan;
 

@@ -63,9 +63,9 @@ def default_tblock(p: "Problem | None" = None) -> int:
     """Temporal blocking factor (0 = off): one history pass feeds this many steps.
 
     Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
-    full / adaptive runs are fastest at 32 (the block kernel turns fp64-tensor
-    bound), short memory and ensembles (per-member coefficient tables built in
-    the CTA) at 24.
+    full memory at 32 (the dense block kernel turns fp64-tensor bound),
+    single-member adaptive at 48 (itemized block stage), short memory and
+    ensembles (per-member coefficient tables built in the CTA) at 24.
     """
     env = os.environ.get("FGB200_TBLOCK")
     if env is not None:
@@ -77,7 +77,11 @@ def default_tblock(p: "Problem | None" = None) -> int:
     # a short memory at least as long as the run is the full schedule, and must
     # give the full schedule's bits (reference property, test_covering_strategies)
     truncating = p.kind == "short" and short_horizon(p.param, float(p.dt[0])) < int(p.n_steps)
-    return 24 if truncating else 32
+    if truncating:
+        return 24
+    # thinned schedules: the itemized block stage does work proportional to the
+    # schedule's terms, so a wider block (fewer history passes) pays off
+    return 48 if p.kind == "adaptive" else 32
 
 
 def round_up(n: int, m: int) -> int:
@@ -303,8 +307,6 @@ class Stepper:
         pool_slices = max(0, len([s for s in self.snap_steps if s > 0]))
         tb = default_tblock(p) if tblock is None else int(tblock)
         p_slices = 2 * tb if tb and n > tb else 0
-        if tb and n > tb and B == 1 and p.kind == "adaptive":
-            p_slices += tb * _lib.FG_MAX_ITEM_ROWS_PER_STEP  # Q
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         free, _total = torch.cuda.mem_get_info(self.device)
         free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
@@ -373,10 +375,7 @@ class Stepper:
                 self.blkcoef = torch.empty((2, rows, _lib.FG_COEF_ROW), **f64)
                 plan.blkcoef_dev = self.blkcoef.data_ptr()
                 plan.coef_rows = rows
-                if p.kind == "adaptive":  # per-item partial sums of the thinned schedule
-                    plan.q_rows = tb * _lib.FG_MAX_ITEM_ROWS_PER_STEP
-                    self.Q = torch.empty((plan.q_rows, slice_elems), **f64)
-                    plan.Q_dev = self.Q.data_ptr()
+
         self.tblock = int(plan.tblock)
         self.plan = plan
         self.k = 0

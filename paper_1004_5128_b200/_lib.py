@@ -24,7 +24,6 @@ FG_RUN_PERSISTENT = 4
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
-FG_MAX_ITEM_ROWS_PER_STEP = 8  # Q rows a step can own (kMaxQ in fg_kernels.cu)
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
 REACTIONS = {"linear": 0, "saturating": 1}

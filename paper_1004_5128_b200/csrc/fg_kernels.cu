@@ -63,7 +63,8 @@ constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit loa
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
-constexpr int kMaxTBlock = 32;  // largest temporal-blocking factor
+constexpr int kMaxTBlock = 64;  // largest temporal-blocking factor (> 32: itemized stages only)
+constexpr int kMaxDenseTBlock = 32;  // largest factor of the dense block kernel
 constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxTBlock + 4)
 
 // ---------------------------------------------------------------- PTX helpers ---
@@ -189,11 +190,40 @@ struct StepArgs {
     int32_t blocked;       // temporal blocking: slices t < kb0 come from P
     int64_t kb0;           // first step of the current block
     const double* P;       // [tblock][B*ms] block partial sums (fg_block_kernel)
-    // blocked mode: schedule weight of offset m (1 <= m <= bb) in the schedule of
-    // step kb0+bb, 0 if absent — the only entries a blocked step still sums
-    // itself, host-evaluated so the step kernel builds no schedule at all
-    uint8_t rw[kMaxTBlock][kMaxTBlock];
+    // blocked single-step launches: the entries of step k's schedule with
+    // 2 <= m <= k-kb0 (the only ones a blocked step still sums itself), host-
+    // evaluated so the step kernel builds no schedule: offsets ascending, weights,
+    // and the weight of m = 1.  Multi-step launches build them on the device.
+    int32_t rn;
+    int32_t rw1;
+    uint8_t rm[kMaxTBlock];
+    uint8_t rwt[kMaxTBlock];
 };
+
+// Recent entries of step k in block kb0 (host and device): offsets 2 <= m <= bb
+// ascending with their weights, and the weight of m = 1 (0 if absent or bb = 0).
+FG_HD int recent_list(int kind, int64_t k, int64_t kb0, int64_t base, int64_t hz, uint8_t* rm, uint8_t* rwt,
+                      int32_t* w1) {
+    FgSeg segs[FG_MAX_SEGS];
+    const int64_t bb = k - kb0;
+    const int n = fg_segments(kind, k, base, hz, segs);
+    int c = 0;
+    *w1 = 0;
+    for (int i = 0; i < n; ++i) {
+        const int64_t st = segs[i].stride;
+        for (int64_t j = 0; j < segs[i].count; ++j) {
+            const int64_t m = segs[i].m0 + j * st;
+            if (m > bb) break;
+            if (m == 1) *w1 = (int32_t)st;
+            if (m >= 2) {
+                rm[c] = (uint8_t)m;
+                rwt[c] = (uint8_t)st;
+                ++c;
+            }
+        }
+    }
+    return c;
+}
 
 // Number of schedule entries with offset m <= mmax (entries ascend in m).
 __device__ __forceinline__ int64_t entries_upto(const FgSeg* s, int n, int64_t mmax) {
@@ -353,33 +383,47 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
         int64_t len, w1;   // schedule length (kinds 0/2), weight of m = 1
         bool has_m1;
         if constexpr (BLK) {
-            w1 = bb >= 1 ? a.rw[bb][1] : 0;
+            // ====== A (temporal blocking): recent slices 2 <= m <= bb only ======
+            // Everything older is in P[bb].  Single-step launches get the recent
+            // entries from the host (no schedule, no shared staging, no CTA
+            // barrier); multi-step launches build them here.  Same entry order
+            // and rounding as the general path.
+            __shared__ uint8_t s_rm[kMaxTBlock], s_rwt[kMaxTBlock];
+            __shared__ int32_t s_rn, s_w1;
+            const uint8_t* rm = a.rm;
+            const uint8_t* rwt = a.rwt;
+            int rn = a.rn;
+            w1 = a.rw1;
+            if (multi) {
+                if (tid == 0) s_rn = recent_list(a.kind, k, a.kb0, a.base, a.hz_max, s_rm, s_rwt, &s_w1);
+                __syncthreads();
+                rm = s_rm;
+                rwt = s_rwt;
+                rn = s_rn;
+                w1 = s_w1;
+            }
             has_m1 = w1 != 0;
             len = k + 1;  // only used for the m = 1 test below (k >= bb >= 1)
-            // ====== A (temporal blocking): recent slices 2 <= m <= bb only ======
-            // Everything older is in P[bb]; the weights come from the host table,
-            // so there is no schedule, no shared staging and no CTA barrier here.
-            // Same entry order and rounding as the general path below.
             for (int p = 0; p < a.passes; ++p) {
                 const int tile = blockIdx.x + p * G;
                 if (tile >= a.total_tiles) break;
                 const int64_t b = tile / a.tpm;
                 const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
                 double acc0 = 0.0, acc1 = 0.0;
-                if (q < a.n_m && bb >= 2) {
+                if (q < a.n_m && rn > 0) {
                     const double* hbase = a.H + b * a.ms + q + k * a.slice_stride;
                     const double* psi_b = a.psi + b * a.psi_stride;
                     const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
-                    const uint8_t* row = a.rw[bb];
                     constexpr int kR = REACT ? 4 : 5;  // recent slices in flight per round (no spills)
 #pragma unroll 1
-                    for (int m0 = 2; m0 <= mmax; m0 += kR) {
+                    for (int e0 = 0; e0 < rn; e0 += kR) {
                         double2 v[kR];
                         double c[kR];
 #pragma unroll
                         for (int u = 0; u < kR; ++u) {
-                            const int m = m0 + u;
-                            const int w = (m <= mmax) ? row[m] : 0;
+                            const int e = e0 + u;
+                            const int m = e < rn ? rm[e] : 0;
+                            const int w = (e < rn && m <= mmax) ? rwt[e] : 0;
                             if (w) {
                                 v[u] = ld_stream(hbase - (int64_t)m * a.slice_stride);
                                 c[u] = __dmul_rn((double)w, __ldg(psi_b + m));
@@ -610,9 +654,11 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 template <bool STAGED>
 __host__ __device__ constexpr int ring_stages() { return STAGED ? FG_STAGED_RING : 4; }
 
-template <int BT, int TP, bool STAGED>
+constexpr int kMainStages = FG_STAGED_RING;  // staged main launches
+constexpr int kTailStages = 2;  // tail launches: small ring, so they fit beside two main CTAs per SM
+
+template <int BT, int TP, bool STAGED, int NS>
 size_t tma_block_smem() {
-    constexpr int NS = ring_stages<STAGED>();
     constexpr int CROWS = STAGED ? NS * kE : kCH;
     return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)CROWS * coef_pitch<BT>() * sizeof(double) +
            (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double) +
@@ -665,9 +711,9 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
 // Coefficients: single member → precomputed rows (fg_block_coef_kernel) copied
 // into the ring with each stage; ensembles (per-member ψ) → a kCH-slice table
 // rebuilt by the consumers at chunk boundaries (scatter over segments).
-template <int BT, int TP, bool STAGED>
+template <int BT, int TP, bool STAGED, int NS>
 __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
-    constexpr int kStages = ring_stages<STAGED>();
+    constexpr int kStages = NS;
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
@@ -845,12 +891,12 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 // j*s (every slice of the block's union is read by exactly the items that use
 // it — one for most slices) and multiplies them with a dense coefficient tile
 // over only its own steps (≈ BT/s), so the work executed is the schedule's
-// terms rounded up to 8-step DMMA tiles.  Items write per-item partial rows
-// Q; a fixed-order reduction sums each step's rows into P (deterministic).
-// Full and short memory are one item (s = 1, every step) written to P directly.
+// terms rounded up to 8-step DMMA tiles.  One CTA per tile walks the items in
+// table order and adds each item's partial sums into the tile's P rows (first
+// item of a step stores), so the sums are deterministic without atomics.  Full
+// and short memory (one class holding every step) keep the dense kernel.
 
 constexpr int kMaxItems = 160;
-constexpr int kMaxQ = 8;        // items a step may appear in (distinct strides)
 constexpr int kItemCols = 8;    // steps per item: one DMMA M tile, so the kernel's
                                 // accumulators (and registers) do not grow with tblock
 constexpr int kItemPitch = kItemCols + 4;  // coefficient row pitch (conflict-free, see coef_pitch)
@@ -859,19 +905,16 @@ struct BlockItem {
     int64_t t_first;
     int32_t stride, n_slices;
     int32_t coef_row;  // first coefficient row (kCoefRow doubles each) of this item
-    int32_t q_row;     // first Q row (direct mode: unused)
+    int32_t first_mask;  // bit c: this item is the first (in table order) to add to step col2step[c]
     int32_t ncols;     // steps in the item (<= kItemCols); column c is step col2step[c]
     uint8_t col2step[kItemCols];
 };
 
 struct ItemTable {
     int32_t n_items;
-    int32_t direct;  // one item holding every step in order: write P rows directly
-    int32_t accumulate;
-    int32_t pad;
+    int32_t accumulate;  // tail launch: every item adds to P (no first stores, no zeroing)
+    uint64_t zero_mask;  // main launch: steps no item touches (their P rows are zeroed)
     BlockItem it[kMaxItems];
-    uint8_t nq[kMaxTBlock];           // Q rows of step b, summed in this order
-    int16_t q[kMaxTBlock][kMaxQ];
 };
 
 // Coefficient rows of every item: row (coef_row + j), column c =
@@ -945,10 +988,10 @@ __device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double*
 // not drain between items): an item's slices are t_first + j*stride, DMMA M
 // tiles beyond its steps are skipped, and its partial sums are flushed from the
 // accumulators when its last stage is done.
-template <int TP>
+template <int TP, int NS>
 __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leave room for two step CTAs
-    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T, double* __restrict__ Q) {
-    constexpr int kStages = ring_stages<true>();
+    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
+    constexpr int kStages = NS;
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = kItemPitch;
     constexpr int MT = 1;
@@ -1008,6 +1051,15 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
     int64_t g = 0;
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
     const int64_t q0 = (int64_t)tile * TP;
+    if (!T.accumulate) {  // steps no item adds to: P = 0 (this CTA owns the tile)
+        for (uint64_t zm = T.zero_mask; zm; zm &= zm - 1) {
+            const int b = __ffsll((long long)zm) - 1;
+            for (int i = tid; i < TP / 2; i += TP) {
+                const int64_t q = q0 + 2 * i;
+                if (q < a.n_m) st_pair(a.P + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
+            }
+        }
+    }
     for (int x = blockIdx.y; x < T.n_items; x += gridDim.y) {
         const BlockItem& it = T.it[x];
         const int mt = (it.ncols + 7) >> 3;
@@ -1025,54 +1077,40 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
             // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
             item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
         }
-        // flush this item's partial sums: row r = step col2step[r]
+        // flush into P (this CTA owns the tile, items in table order, so the
+        // sum of each step is deterministic): the first item of a step stores,
+        // later ones (and every tail item) add — loads first, one round trip.
+        // A step's row can sit in another lane than in the previous item (only
+        // this warp touches these points): the warp barrier orders the accesses.
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
             const int r = 8 * i + fr;
             if (i >= mt || r >= it.ncols) continue;
-            double* out = T.direct ? a.P + (int64_t)it.col2step[r] * a.slice_stride
-                                   : Q + ((int64_t)it.q_row + r) * a.slice_stride;
+            double* out = a.P + (int64_t)it.col2step[r] * a.slice_stride;
+            const bool add = T.accumulate || !((it.first_mask >> r) & 1);
+            double2 old[NT];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
+                old[j] = (add && q < a.n_m) ? ld_cg2(out + q) : make_double2(0.0, 0.0);
+            }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
                 if (q >= a.n_m) continue;
-                double* o = out + q;
-                if (T.direct && T.accumulate) {
-                    const double2 old = ld_cg2(o);
-                    st_pair(o, __dadd_rn(old.x, d[i][j][0]), __dadd_rn(old.y, d[i][j][1]));
-                } else {
-                    st_pair(o, d[i][j][0], d[i][j][1]);
-                }
+                if (add)
+                    st_pair(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]));
+                else
+                    st_pair(out + q, d[i][j][0], d[i][j][1]);
             }
         }
     }
     }  // tiles
 }
 
-// P[b] = Σ of step b's item rows of Q, in the table's fixed order.
-__global__ void fg_item_reduce_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
-                                      const double* __restrict__ Q) {
-    const int b = blockIdx.y;
-    const int64_t pairs = (a.n_m + 1) / 2;
-    const int n = T.nq[b];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int r = 0; r < n; ++r) {
-            const double2 v = ld_cg2(Q + (int64_t)T.q[b][r] * a.slice_stride + 2 * i);
-            if (r == 0) {
-                acc = v;
-            } else {
-                acc.x = __dadd_rn(acc.x, v.x);
-                acc.y = __dadd_rn(acc.y, v.y);
-            }
-        }
-        st_pair(a.P + (int64_t)b * a.slice_stride + 2 * i, acc.x, acc.y);
-    }
-}
-
-template <int TP>
+template <int TP, int NS>
 size_t item_block_smem() {
-    constexpr int NS = ring_stages<true>();
     return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * kItemPitch * sizeof(double) +
            (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
 }
@@ -1178,8 +1216,12 @@ int validate_plan(const fg_plan* p) {
         return fail(FG_ERR_ARG, "plan has a NULL device pointer");
     if (p->split != 0 && p->split != 1 && p->split != 2 && p->split != 4 && p->split != 8)
         return fail(FG_ERR_ARG, "split must be 0, 1, 2, 4 or 8");
-    if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16 && p->tblock != 24 && p->tblock != 32)
-        return fail(FG_ERR_ARG, "tblock must be 0, 8, 16, 24 or 32");
+    if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16 && p->tblock != 24 && p->tblock != 32 &&
+        p->tblock != 48 && p->tblock != 64)
+        return fail(FG_ERR_ARG, "tblock must be 0, 8, 16, 24, 32, 48 or 64");
+    if (p->tblock > kMaxDenseTBlock && (p->B != 1 || p->kind != FG_MEM_ADAPTIVE || !p->blkcoef_dev))
+        return fail(FG_ERR_UNSUPPORTED, "tblock %d needs a single-member adaptive plan with blkcoef_dev",
+                    (int)p->tblock);
     if (p->tblock && !p->P_dev) return fail(FG_ERR_ARG, "temporal blocking needs P_dev");
     if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
         FgSeg s[FG_MAX_SEGS];
@@ -1303,13 +1345,8 @@ double* block_coef(const fg_plan* p, int64_t kb0) {
 
 // Recent-weight rows of a temporal block: a.rw[k-kb0][m] = weight of offset m in
 // the schedule of step k (1 <= m <= k-kb0), for k in [k0, k1).
-void fill_recent(StepArgs& a, const fg_plan* p, int64_t kb0, int64_t k0, int64_t k1) {
-    FgSeg segs[FG_MAX_SEGS];
-    for (int64_t k = k0; k < k1; ++k) {
-        const int64_t bb = k - kb0;
-        const int n = fg_segments(p->kind, k, p->base, a.hz_max, segs);
-        for (int64_t m = 1; m <= bb && n > 0; ++m) a.rw[bb][m] = (uint8_t)fg_seg_weight(segs, n, m);
-    }
+void fill_recent(StepArgs& a, const fg_plan* p, int64_t kb0, int64_t k) {
+    a.rn = recent_list(p->kind, k, kb0, p->base, a.hz_max, a.rm, a.rwt, &a.rw1);
 }
 
 // Ask for the largest shared-memory carveout for every kernel of the pipeline so
@@ -1348,7 +1385,7 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
         a.blocked = 1;
         a.kb0 = kb0;
         a.P = block_P(p, kb0);
-        fill_recent(a, p, kb0, k, k + 1);
+        fill_recent(a, p, kb0, k);
     }
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s, kb0 >= 0);
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
@@ -1375,13 +1412,13 @@ struct BlockVariant {
     int tp;
 };
 
-template <int BT, bool ST>
+template <int BT, bool ST, int NS>
 BlockVariant block_variant(int tp) {
     switch (tp) {
-        case 128: return {fg_block_tma_kernel<BT, 128, ST>, tma_block_smem<BT, 128, ST>(), 128};
-        case 192: return {fg_block_tma_kernel<BT, 192, ST>, tma_block_smem<BT, 192, ST>(), 192};
-        case 224: return {fg_block_tma_kernel<BT, 224, ST>, tma_block_smem<BT, 224, ST>(), 224};
-        default: return {fg_block_tma_kernel<BT, 256, ST>, tma_block_smem<BT, 256, ST>(), 256};
+        case 128: return {fg_block_tma_kernel<BT, 128, ST, NS>, tma_block_smem<BT, 128, ST, NS>(), 128};
+        case 192: return {fg_block_tma_kernel<BT, 192, ST, NS>, tma_block_smem<BT, 192, ST, NS>(), 192};
+        case 224: return {fg_block_tma_kernel<BT, 224, ST, NS>, tma_block_smem<BT, 224, ST, NS>(), 224};
+        default: return {fg_block_tma_kernel<BT, 256, ST, NS>, tma_block_smem<BT, 256, ST, NS>(), 256};
     }
 }
 
@@ -1389,7 +1426,14 @@ BlockVariant block_variant(int tp) {
 // HBM), so pick the TP (32-point warps, 4..8 per CTA) that minimises the work of
 // the busiest SM, ceil(tiles / SMs) * TP; c2 (65536 points) gets 293 tiles of
 // 224 instead of 256 tiles of 256 that leave 40 SMs half idle.
-BlockVariant choose_block_variant(const fg_plan* p) {
+template <int BT>
+BlockVariant block_variant_of(bool staged, bool tail, int tp) {
+    if (tail) return staged ? block_variant<BT, true, kTailStages>(tp) : block_variant<BT, false, kTailStages>(tp);
+    return staged ? block_variant<BT, true, kMainStages>(tp) : block_variant<BT, false, ring_stages<false>()>(tp);
+}
+
+// tail: the variant with the small ring (see kTailStages)
+BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
     static const char* force = getenv("FGB200_BLOCK_TP");
     const int cands[4] = {256, 224, 192, 128};
     const bool staged = p->B == 1 && p->blkcoef_dev;
@@ -1403,10 +1447,10 @@ BlockVariant choose_block_variant(const fg_plan* p) {
         if (cost < best_cost) {
             best_cost = cost;
             switch (p->tblock) {
-                case 8: best = staged ? block_variant<8, true>(tp) : block_variant<8, false>(tp); break;
-                case 24: best = staged ? block_variant<24, true>(tp) : block_variant<24, false>(tp); break;
-                case 32: best = staged ? block_variant<32, true>(tp) : block_variant<32, false>(tp); break;
-                default: best = staged ? block_variant<16, true>(tp) : block_variant<16, false>(tp); break;
+                case 8: best = block_variant_of<8>(staged, tail, tp); break;
+                case 24: best = block_variant_of<24>(staged, tail, tp); break;
+                case 32: best = block_variant_of<32>(staged, tail, tp); break;
+                default: best = block_variant_of<16>(staged, tail, tp); break;
             }
         }
     }
@@ -1500,7 +1544,7 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
     // streams it once for all steps; items would re-read it per 8 steps
     if (ng == 1 && g[0].s == 1 && g[0].n == bt && bt > kItemCols) return false;
     int n = 0;
-    int64_t crow = row0, qrow = 0;
+    int64_t crow = row0;
     for (int x = 0; x < ng; ++x) {
         for (int c0 = 0; c0 < g[x].n; c0 += kItemCols) {
             if (n == kMaxItems) return false;
@@ -1512,60 +1556,57 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
             for (int c = 0; c < it.ncols; ++c) it.col2step[c] = g[x].cols[c0 + c];
             it.coef_row = (int32_t)crow;
             crow += it.n_slices;
-            it.q_row = (int32_t)qrow;
-            qrow += it.ncols;
         }
     }
     T.n_items = n;
-    T.direct = n == 1 && T.it[0].ncols == bt;  // columns are appended in step order
-    for (int b = 0; b < bt && !T.direct; ++b) {
-        for (int x = 0; x < n; ++x) {
-            const BlockItem& it = T.it[x];
-            for (int c = 0; c < it.ncols; ++c)
-                if (it.col2step[c] == b) {
-                    if (T.nq[b] == kMaxQ) return false;
-                    T.q[b][T.nq[b]++] = (int16_t)(it.q_row + c);
-                }
+    uint64_t seen = 0;
+    for (int x = 0; x < n; ++x) {
+        BlockItem& it = T.it[x];
+        for (int c = 0; c < it.ncols; ++c) {
+            const uint64_t bit = 1ull << it.col2step[c];
+            if (!(seen & bit)) it.first_mask |= 1 << c;
+            seen |= bit;
         }
     }
+    T.zero_mask = ~seen & (bt >= 64 ? ~0ull : ((1ull << bt) - 1));
     if (crow * kItemPitch > coef_capacity(p)) return false;
-    if (!T.direct && (!p->Q_dev || qrow > p->q_rows)) return false;
     return true;
 }
 
-int launch_items(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st) {
-    double* rows = const_cast<double*>(a.gcoef);
+int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
+    if (T.n_items == 0) return FG_OK;
     int max_rows = 0;
     for (int x = 0; x < T.n_items; ++x) max_rows = T.it[x].n_slices > max_rows ? T.it[x].n_slices : max_rows;
     const int cx = (max_rows * kItemPitch + 255) / 256;
-    fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items), 256, 0, st>>>(a, T, rows);
-    if (int rc = cuda_check(cudaGetLastError(), "fg_item_coef launch")) return rc;
-    void (*kern)(const BlockArgs, const ItemTable, double*) = nullptr;
+    fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items), 256, 0, st>>>(
+        a, T, const_cast<double*>(a.gcoef));
+    return cuda_check(cudaGetLastError(), "fg_item_coef launch");
+}
+
+// Item partial sums (coefficient rows already built) into Q, then the ordered
+// reduction into P (or directly into P for a single all-steps item).
+int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st,
+                     bool tail = false) {
+    void (*kern)(const BlockArgs, const ItemTable) = nullptr;
     size_t smem = 0;
     switch (tp) {
-        case 128: kern = fg_block_item_kernel<128>; smem = item_block_smem<128>(); break;
-        case 192: kern = fg_block_item_kernel<192>; smem = item_block_smem<192>(); break;
-        case 224: kern = fg_block_item_kernel<224>; smem = item_block_smem<224>(); break;
-        default: kern = fg_block_item_kernel<256>; smem = item_block_smem<256>(); tp = 256; break;
+        case 128: kern = tail ? fg_block_item_kernel<128, kTailStages> : fg_block_item_kernel<128, kMainStages>;
+                  smem = tail ? item_block_smem<128, kTailStages>() : item_block_smem<128, kMainStages>(); break;
+        case 192: kern = tail ? fg_block_item_kernel<192, kTailStages> : fg_block_item_kernel<192, kMainStages>;
+                  smem = tail ? item_block_smem<192, kTailStages>() : item_block_smem<192, kMainStages>(); break;
+        case 224: kern = tail ? fg_block_item_kernel<224, kTailStages> : fg_block_item_kernel<224, kMainStages>;
+                  smem = tail ? item_block_smem<224, kTailStages>() : item_block_smem<224, kMainStages>(); break;
+        default: kern = tail ? fg_block_item_kernel<256, kTailStages> : fg_block_item_kernel<256, kMainStages>;
+                 smem = tail ? item_block_smem<256, kTailStages>() : item_block_smem<256, kMainStages>(); tp = 256; break;
     }
     if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                             "item smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
-    // FGB200_ITEM_GRID=1: one CTA per (tile, item); default: one CTA per tile
-    // (at most FGB200_BLOCK_CTAS_PER_SM per SM) walks all items
-    const char* ig = getenv("FGB200_ITEM_GRID");
-    const bool per_item = ig && ig[0] == '1';
-    const dim3 grid = per_item ? dim3((unsigned)a.total_tiles, (unsigned)T.n_items) : dim3(block_grid(p, a.total_tiles));
-    kern<<<grid, tp + 32, smem, st>>>(a, T, p->Q_dev);
-    if (int rc = cuda_check(cudaGetLastError(), "fg_block_item launch")) return rc;
-    if (!T.direct) {
-        const int64_t pairs = (p->n_m + 1) / 2;
-        const unsigned gx = (unsigned)((pairs + 255) / 256 < 256 ? (pairs + 255) / 256 : 256);
-        fg_item_reduce_kernel<<<dim3(gx, (unsigned)a.bt), 256, 0, st>>>(a, T, p->Q_dev);
-        if (int rc = cuda_check(cudaGetLastError(), "fg_item_reduce launch")) return rc;
-    }
-    return FG_OK;
+    // one CTA per tile (at most FGB200_BLOCK_CTAS_PER_SM per SM) walks all items:
+    // it owns the tile's P rows, so the items' adds need no atomics
+    kern<<<block_grid(p, a.total_tiles), tp + 32, smem, st>>>(a, T);
+    return cuda_check(cudaGetLastError(), "fg_block_item launch");
 }
 
 // Dense coefficient rows (fg_block_coef_kernel) of slices [a.t_begin, a.t_end)
@@ -1595,11 +1636,17 @@ bool items_enabled() {
     return !(e && e[0] == '0');
 }
 
+// Tail launches of factors above kMaxDenseTBlock are itemized too (the dense
+// kernel's accumulators would not fit).
+bool item_tail(const fg_plan* p) { return p->tblock > kMaxDenseTBlock; }
+
+int64_t tail_begin(const fg_plan* p, int64_t kb0) { return kb0 - p->tblock > 0 ? kb0 - p->tblock : 0; }
+
 // main launch: P = Σ over slices t < kb0 - tblock (all but the previous block's).
 // Everything it reads is final once the previous block starts, so fg_run
 // issues it on a side stream while the previous block's steps run.  Single
-// member: coefficient buffer = [tail rows (tblock)][main rows]; the tail rows
-// are built here too so the tail launch (on the critical path) only multiplies.
+// member: coefficient buffer = [tail rows][main rows]; the tail's rows are
+// built here too so the tail launch (on the critical path) only multiplies.
 int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (kb0 <= 0) {  // nothing older than the block: P = 0
         return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
@@ -1609,21 +1656,37 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
     BlockArgs a = block_args(p, kb0, bt, v);
     a.t_begin = 0;
-    a.t_end = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
+    a.t_end = tail_begin(p, kb0);
     if (a.gcoef) {
-        const int64_t cp = p->tblock + 4;
-        BlockArgs tail = a;  // tail rows at the buffer start
-        tail.t_begin = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
+        int64_t row0 = 0;  // main rows start after the tail's (in item-pitch rows when itemized)
+        BlockArgs tail = a;
+        tail.t_begin = tail_begin(p, kb0);
         tail.t_end = kb0;
-        if (int rc = launch_dense_coef(p, tail, st)) return rc;
-        a.gcoef += p->tblock * cp;
+        if (item_tail(p)) {
+            ItemTable Tt;
+            if (!build_items(p, kb0, bt, tail.t_begin, tail.t_end, Tt, 0))
+                return fail(FG_ERR_UNSUPPORTED, "tblock %d: tail of block %lld does not fit the item table",
+                            (int)p->tblock, (long long)kb0);
+            if (int rc = launch_item_coef(tail, Tt, st)) return rc;
+            for (int x = 0; x < Tt.n_items; ++x) row0 += Tt.it[x].n_slices;
+        } else {
+            if (int rc = launch_dense_coef(p, tail, st)) return rc;
+            const int64_t cp = p->tblock + 4;
+            row0 = (p->tblock * cp + kItemPitch - 1) / kItemPitch;  // dense tail rows, in item-pitch rows
+        }
         ItemTable T;
-        if (items_enabled() && build_items(p, kb0, bt, 0, a.t_end, T, 0)) {
+        const bool ok = items_enabled() || item_tail(p);
+        if (ok && build_items(p, kb0, bt, 0, a.t_end, T, row0)) {
             if (T.n_items == 0)
                 return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->ms * sizeof(double), st),
                                   "P reset");
-            return launch_items(p, a, T, v.tp, st);
+            if (int rc = launch_item_coef(a, T, st)) return rc;
+            return launch_item_sums(p, a, T, v.tp, st);
         }
+        if (item_tail(p))
+            return fail(FG_ERR_UNSUPPORTED, "tblock %d: block %lld does not fit the item table", (int)p->tblock,
+                        (long long)kb0);
+        a.gcoef += row0 * kItemPitch;
         if (int rc = launch_dense_coef(p, a, st)) return rc;
     }
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
@@ -1638,18 +1701,73 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
 // stream order after that block's last step and this block's main launch.
 int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (kb0 <= 0) return FG_OK;
-    const BlockVariant v = choose_block_variant(p);
+    const BlockVariant v = choose_block_variant(p, true);
     if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
     BlockArgs a = block_args(p, kb0, bt, v);
-    a.t_begin = kb0 - p->tblock > 0 ? kb0 - p->tblock : 0;
+    a.t_begin = tail_begin(p, kb0);
     a.t_end = kb0;
     a.accumulate = 1;
+    if (item_tail(p)) {
+        ItemTable T;
+        if (!build_items(p, kb0, bt, a.t_begin, a.t_end, T, 0))
+            return fail(FG_ERR_UNSUPPORTED, "tblock %d: tail of block %lld does not fit the item table",
+                        (int)p->tblock, (long long)kb0);
+        if (T.n_items == 0) return FG_OK;
+        T.accumulate = 1;
+        return launch_item_sums(p, a, T, v.tp, st, true);
+    }
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
         return rc;
+    if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
     v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
+
+// Debug timeline of the temporal-blocking pipeline (FGB200_TRACE=<file>, not in
+// graph mode): per block, timed events at its start (0), after the join (1),
+// after its tail (2), and around the next block's main launch on the side
+// stream (3, 4); fg_run synchronises at the end and appends one line per block.
+struct BlockTrace {
+    const char* path;
+    std::vector<int64_t> kb;
+    std::vector<cudaEvent_t> ev;  // 5 per block
+    explicit BlockTrace(const char* p) : path(p) {}
+    void mark(int64_t k, int slot, cudaStream_t s) {
+        if (!path) return;
+        if (kb.empty() || kb.back() != k) {
+            kb.push_back(k);
+            ev.resize(ev.size() + 5, nullptr);
+        }
+        cudaEvent_t& e = ev[(kb.size() - 1) * 5 + slot];
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+    }
+    void dump(cudaStream_t s) {
+        if (!path || kb.empty()) return;
+        cudaEvent_t fin;
+        cudaEventCreate(&fin);
+        cudaEventRecord(fin, s);
+        cudaEventSynchronize(fin);
+        cudaDeviceSynchronize();
+        FILE* f = fopen(path, "a");
+        auto ms = [](cudaEvent_t a, cudaEvent_t b) {
+            float t = 0.f;
+            if (a && b) cudaEventElapsedTime(&t, a, b);
+            return t * 1e3f;
+        };
+        for (size_t i = 0; f && i < kb.size(); ++i) {
+            cudaEvent_t* e = &ev[i * 5];
+            cudaEvent_t next = i + 1 < kb.size() ? ev[(i + 1) * 5] : fin;
+            fprintf(f, "%lld t=%.1f wait=%.1f tail=%.1f steps=%.1f main_next=%.1f\n", (long long)kb[i],
+                    ms(ev[0], e[0]), ms(e[0], e[1]), ms(e[1], e[2]), ms(e[2], next), ms(e[3], e[4]));
+        }
+        if (f) fclose(f);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        cudaEventDestroy(fin);
+    }
+};
 
 // FGB200_BLOCK_OVERLAP=0 turns the side-stream pipeline off (same results).
 bool overlap_enabled() {
@@ -1740,7 +1858,6 @@ int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cu
         a.blocked = 1;
         a.kb0 = kb0;
         a.P = block_P(p, kb0);
-        fill_recent(a, p, kb0, k0, k1);
     }
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s, kb0 >= 0);
     const size_t smem = acc_smem(s, passes);
@@ -1981,6 +2098,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
         if (overlap_enabled()) rc = side_stream(&side, &ev_fork, ev_join);
         int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
+        BlockTrace tr(graph ? nullptr : getenv("FGB200_TRACE"));
         for (int64_t kb = k0 - k0 % tb; kb < k1 && rc == FG_OK; kb += tb) {
             const int64_t ks = kb > k0 ? kb : k0, ke = kb + tb < k1 ? kb + tb : k1;
             // blocks are aligned to multiples of tb, so a run split into several
@@ -1989,10 +2107,13 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
             if (start) {
                 const int64_t nk = kb + tb;
                 const bool fork_next = side && nk < k1;
+                tr.mark(kb, 0, cap);
                 if (fork_next) {
                     rc = cuda_check(cudaEventRecord(ev_fork, cap), "fork record");
                     if (rc == FG_OK) rc = cuda_check(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+                    tr.mark(kb, 3, side);
                     if (rc == FG_OK) rc = launch_block_main(p, nk, block_len(nk), side);
+                    tr.mark(kb, 4, side);
                     if (rc == FG_OK) rc = cuda_check(cudaEventRecord(ev_join[(nk / tb) & 1], side), "join record");
                     if (rc != FG_OK) break;
                 }
@@ -2001,7 +2122,9 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
                 else
                     rc = launch_block_main(p, kb, block_len(kb), cap);
                 main_on_side = fork_next ? nk : -1;
+                tr.mark(kb, 1, cap);
                 if (rc == FG_OK) rc = launch_block_tail(p, kb, block_len(kb), cap);
+                tr.mark(kb, 2, cap);
                 if (rc != FG_OK) break;
             }
             rc = persistent ? persistent_steps(ks, ke, kb) : steps(ks, ke, kb, start);
@@ -2011,6 +2134,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
                 cuda_check(cudaStreamWaitEvent(cap, ev_join[(main_on_side / tb) & 1], 0), "join side stream");
             if (rc == FG_OK) rc = r2;
         }
+        tr.dump(cap);
     }
 
     if (cstream) {  // join the copies: a sync of `stream` covers the host snapshots

@@ -29,7 +29,7 @@ def expected_partials(H, kind, param, kb0, bt, table, dt=1.0):
     ((256, 256), "adaptive", 5), ((256, 256), "full", 0), ((48, 48), "adaptive", 3), ((4096,), "full", 0),
     ((300,), "adaptive", 2), ((64, 64), "short", 37.0)])
 @pytest.mark.parametrize("kb0,bt", [(16, 16), (160, 16), (1030, 16), (2000, 7), (517, 8), (48, 24), (1200, 24),
-                                    (999, 32)])
+                                    (999, 32), (64, 64), (1280, 64), (1000, 48)])
 def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     import torch
 
@@ -37,7 +37,9 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     from paper_1004_5128_b200 import _lib
     from paper_1004_5128_b200._engine import Stepper
 
-    tblock = {8: 8, 24: 24, 32: 32}.get(bt, 16)
+    tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64}.get(bt, 16)
+    if tblock > 32 and kind != "adaptive":
+        pytest.skip("factors above 32 are single-member adaptive only")
     n_steps = kb0 + bt + 1
     u0 = np.zeros(shape)
     strat = {"full": lambda: fg.FullMemory(), "short": lambda: fg.ShortMemory(param),

@@ -410,6 +410,22 @@ def test_temporal_blocking_matches_goldens(fg, golden, name, tblock):
             assert err <= TOL, f"{name} tblock {tblock} member {b} step {s}: {err:.3e}"
 
 
+ADAPTIVE_SINGLE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_adaptive4"]
+
+
+@pytest.mark.parametrize("tblock", [48, 64])
+@pytest.mark.parametrize("name", ADAPTIVE_SINGLE)
+def test_wide_temporal_blocking_matches_goldens(fg, golden, name, tblock):
+    """Factors above 32 (itemized main and tail launches, single-member adaptive)."""
+    test_temporal_blocking_matches_goldens(fg, golden, name, tblock)
+
+
+def test_wide_temporal_blocking_rejects_dense_plans(fg, golden):
+    cfg = _any_field_config(fg, golden, "point_full")
+    with pytest.raises(ValueError, match="tblock 64"):
+        fg.run_field(cfg, tblock=64)
+
+
 @pytest.mark.parametrize("name", ["c2_small", "batch_short", "3d_sat_full"])
 def test_temporal_blocking_modes_bitwise(fg, golden, name, monkeypatch):
     """Blocked runs are identical across launch modes (side-stream pipeline on
