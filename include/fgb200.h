@@ -107,6 +107,9 @@ int fg_abi_version(void);
 /* sizeof(fg_plan) as compiled into the library (binding layout check). */
 int64_t fg_plan_sizeof(void);
 const char* fg_last_error(void);
+/* Kernels this library has launched from the calling thread so far (graph mode:
+ * kernel nodes captured); for launch accounting (bench.py gpu_launches). */
+int64_t fg_kernel_launches(void);
 /* 0 on success; fills the SM count and compute capability of the current device. */
 int fg_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 

@@ -30,7 +30,7 @@ REACTIONS = {"linear": 0, "saturating": 1}
 
 # every symbol include/fgb200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
-    "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
+    "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_kernel_launches", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
     "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_run_ex", "fg_status",
     "fg_step_geometry", "fg_block_union", "fg_block_partials",
 )
@@ -91,6 +91,7 @@ def _declare(L):
         "fg_abi_version": (C.c_int, []),
         "fg_plan_sizeof": (C.c_int64, []),
         "fg_last_error": (C.c_char_p, []),
+        "fg_kernel_launches": (C.c_int64, []),
         "fg_device_info": (C.c_int, [_p32, _p32, _p32]),
         "fg_psi_tables": (C.c_int, [vp, i64, i64, i64, vp, vp]),
         "fg_schedule_len": (C.c_int, [i32, i64, i64, i64, _p64]),

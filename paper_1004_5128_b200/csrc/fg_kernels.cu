@@ -40,6 +40,7 @@
 namespace {
 
 thread_local std::string g_last_error;
+thread_local int64_t g_launches = 0;  // kernels this thread has launched (fg_kernel_launches)
 
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
@@ -1401,6 +1402,7 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
+    ++g_launches;
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step launch");
 }
 
@@ -1578,6 +1580,7 @@ int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
     int max_rows = 0;
     for (int x = 0; x < T.n_items; ++x) max_rows = T.it[x].n_slices > max_rows ? T.it[x].n_slices : max_rows;
     const int cx = (max_rows * kItemPitch + 255) / 256;
+    ++g_launches;
     fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items), 256, 0, st>>>(
         a, T, const_cast<double*>(a.gcoef));
     return cuda_check(cudaGetLastError(), "fg_item_coef launch");
@@ -1605,6 +1608,7 @@ int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, i
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
     // one CTA per tile (at most FGB200_BLOCK_CTAS_PER_SM per SM) walks all items:
     // it owns the tile's P rows, so the items' adds need no atomics
+    ++g_launches;
     kern<<<block_grid(p, a.total_tiles), tp + 32, smem, st>>>(a, T);
     return cuda_check(cudaGetLastError(), "fg_block_item launch");
 }
@@ -1622,10 +1626,10 @@ int launch_dense_coef(const fg_plan* p, const BlockArgs& a, cudaStream_t st) {
                             "coefficient rows reset"))
         return rc;
     switch (p->tblock) {
-        case 8: fg_block_coef_kernel<8><<<a.bt, 256, 0, st>>>(a, rows); break;
-        case 24: fg_block_coef_kernel<24><<<a.bt, 256, 0, st>>>(a, rows); break;
-        case 32: fg_block_coef_kernel<32><<<a.bt, 256, 0, st>>>(a, rows); break;
-        default: fg_block_coef_kernel<16><<<a.bt, 256, 0, st>>>(a, rows); break;
+        case 8: ++g_launches; fg_block_coef_kernel<8><<<a.bt, 256, 0, st>>>(a, rows); break;
+        case 24: ++g_launches; fg_block_coef_kernel<24><<<a.bt, 256, 0, st>>>(a, rows); break;
+        case 32: ++g_launches; fg_block_coef_kernel<32><<<a.bt, 256, 0, st>>>(a, rows); break;
+        default: ++g_launches; fg_block_coef_kernel<16><<<a.bt, 256, 0, st>>>(a, rows); break;
     }
     return cuda_check(cudaGetLastError(), "fg_block_coef launch");
 }
@@ -1693,6 +1697,7 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
                             "block smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
+    ++g_launches;
     v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
@@ -1720,6 +1725,7 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
                             "block smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
+    ++g_launches;
     v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
@@ -1877,6 +1883,7 @@ int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cu
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    ++g_launches;
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step persistent launch");
 }
 
@@ -1887,6 +1894,8 @@ int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cu
 extern "C" {
 
 int fg_abi_version(void) { return FGB200_ABI_VERSION; }
+
+int64_t fg_kernel_launches(void) { return g_launches; }
 
 int64_t fg_plan_sizeof(void) { return (int64_t)sizeof(fg_plan); }
 
@@ -1915,6 +1924,7 @@ int fg_psi_tables(const double* gamma_dev, int64_t B, int64_t n, int64_t stride,
     if (!gamma_dev || !out_dev || B < 1 || n < 0 || stride < n + 1)
         return fail(FG_ERR_ARG, "fg_psi_tables: bad arguments");
     const int threads = 128;
+    ++g_launches;
     fg_psi_kernel<<<(unsigned)((B + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
         gamma_dev, B, n, stride, out_dev);
     return cuda_check(cudaGetLastError(), "fg_psi_kernel");
@@ -1934,6 +1944,7 @@ int fg_schedule_expand(int32_t kind, int64_t k0, int64_t nk, int64_t base, int64
         return fail(FG_ERR_ARG, "fg_schedule_expand: bad arguments");
     FgSeg s[FG_MAX_SEGS];
     if (fg_segments(kind, k0, base, horizon, s) < 0) return fail(FG_ERR_ARG, "fg_schedule_expand: invalid schedule");
+    ++g_launches;
     fg_schedule_kernel<<<(unsigned)nk, 128, 0, (cudaStream_t)stream>>>(kind, k0, base, horizon, offs, wts,
                                                                         row_cap, lens);
     return cuda_check(cudaGetLastError(), "fg_schedule_kernel");
@@ -1945,6 +1956,7 @@ int fg_history_sum(const double* H, int64_t ss, int64_t n, const int64_t* offs, 
         return fail(FG_ERR_ARG, "fg_history_sum: bad arguments");
     (void)psi_len;  // bounds are validated by the host before the call (solver.py:177-189)
     const int threads = 256;
+    ++g_launches;
     fg_history_sum_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
         H, ss, n, offs, wts, len, psi, k, out);
     return cuda_check(cudaGetLastError(), "fg_history_sum_kernel");
@@ -1957,6 +1969,7 @@ int fg_stencil(const fg_plan* p, const double* u, double* out, void* stream) {
     dim3 grid((unsigned)((p->n_m + threads - 1) / threads), (unsigned)p->B);
     const Shape sh = shape_of(p);
     cudaStream_t st = (cudaStream_t)stream;
+    ++g_launches;
     if (p->ndim == 1)
         fg_stencil_kernel<1><<<grid, threads, 0, st>>>(u, out, p->B, p->ms, (int32_t)p->n_m, sh);
     else if (p->ndim == 2)
