@@ -81,7 +81,8 @@ def default_tblock(p: "Problem | None" = None) -> int:
         return 24
     # thinned schedules: the itemized block stage does work proportional to the
     # schedule's terms, so a wider block (fewer history passes) pays off
-    return 48 if p.kind == "adaptive" else 32
+    thinned = p.kind == "adaptive" and int(p.param) < int(p.n_steps)  # base >= n: the full schedule
+    return 48 if thinned else 32
 
 
 def round_up(n: int, m: int) -> int:

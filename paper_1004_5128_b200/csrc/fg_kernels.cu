@@ -132,8 +132,54 @@ __device__ __forceinline__ bool interior(const Shape& sh, int32_t q) {
     return i0 > 0 && i0 < sh.n0 - 1 && i1 > 0 && i1 < sh.n1 - 1 && i2 > 0 && i2 < sh.n2 - 1;
 }
 
+// Interior flags of the point pair (q, q+1) from one coordinate decomposition
+// (the per-point `interior` costs an integer division per axis).
+template <int NDIM>
+__device__ __forceinline__ void interior_pair(const Shape& sh, int32_t q, bool& in0, bool& in1) {
+    if (NDIM == 1) {
+        in0 = q > 0 && q < sh.n0 - 1;
+        in1 = q + 1 > 0 && q + 1 < sh.n0 - 1;
+    } else if (NDIM == 2) {
+        const int32_t j = q / sh.n1, l = q - j * sh.n1;
+        const bool row = j > 0 && j < sh.n0 - 1;
+        in0 = row && l > 0 && l < sh.n1 - 1;
+        // q+1 in the same row unless l is the last column (then it is a ring point)
+        in1 = row && l + 1 < sh.n1 - 1;
+    } else {
+        const int32_t plane = sh.n1 * sh.n2;
+        const int32_t i0 = q / plane, r = q - i0 * plane;
+        const int32_t i1 = r / sh.n2, i2 = r - i1 * sh.n2;
+        const bool line = i0 > 0 && i0 < sh.n0 - 1 && i1 > 0 && i1 < sh.n1 - 1;
+        in0 = line && i2 > 0 && i2 < sh.n2 - 1;
+        in1 = line && i2 + 1 < sh.n2 - 1;
+    }
+}
+
 // u is read through L2 (.cg): in the persistent kernel the field buffers are
 // rewritten every other step, so an L1 copy could be stale.
+template <int NDIM>
+__device__ __forceinline__ double delta_in(const double* __restrict__ u, const Shape& sh, int32_t q, double c,
+                                           bool in) {
+    if (!in) return 0.0;
+    if (NDIM == 1) {
+        return __dsub_rn(__dadd_rn(ld_cg(u + q + 1), ld_cg(u + q - 1)), __dmul_rn(2.0, c));
+    } else if (NDIM == 2) {
+        const int32_t sx = sh.n1;
+        double r = __dadd_rn(ld_cg(u + q + sx), ld_cg(u + q - sx));
+        r = __dsub_rn(r, __dmul_rn(4.0, c));
+        r = __dadd_rn(r, ld_cg(u + q + 1));
+        return __dadd_rn(r, ld_cg(u + q - 1));
+    } else {
+        const int32_t sy = sh.n2, sx = sh.n1 * sh.n2;
+        double r = __dadd_rn(ld_cg(u + q + sx), ld_cg(u + q - sx));
+        r = __dsub_rn(r, __dmul_rn(6.0, c));
+        r = __dadd_rn(r, ld_cg(u + q + sy));
+        r = __dadd_rn(r, ld_cg(u + q - sy));
+        r = __dadd_rn(r, ld_cg(u + q + 1));
+        return __dadd_rn(r, ld_cg(u + q - 1));
+    }
+}
+
 template <int NDIM>
 __device__ __forceinline__ double delta_at(const double* __restrict__ u, const Shape& sh, int32_t q,
                                            double c) {
@@ -482,14 +528,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 const double* psi_b = a.psi + b * a.psi_stride;
                 const double2 uu = ld_cg2(ub + q);
                 const double u0 = uu.x, u1 = uu.y;
+                bool in0, in1;
+                interior_pair<NDIM>(a.sh, q, in0, in1);
+                in1 = in1 && q + 1 < a.n_m;
                 double d0, d1;
                 if (a.m0_from_history) {
                     const double2 h = ld_cg2(a.H + k * a.slice_stride + moff);
                     d0 = h.x;
                     d1 = h.y;
                 } else {
-                    d0 = delta_at<NDIM>(ub, a.sh, q, u0);
-                    d1 = (q + 1 < a.n_m) ? delta_at<NDIM>(ub, a.sh, q + 1, u1) : 0.0;
+                    d0 = delta_in<NDIM>(ub, a.sh, q, u0, in0);
+                    d1 = delta_in<NDIM>(ub, a.sh, q + 1, u1, in1);
                     if (live) st_pair(a.H + k * a.slice_stride + moff, d0, d1);
                 }
                 const double2 part = s_acc[p * kLanes + slot];
@@ -524,8 +573,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                     n0 = __dadd_rn(__dadd_rn(u0, __dmul_rn(dt, f0)), __dmul_rn(diffuse, acc0));
                     n1 = __dadd_rn(__dadd_rn(u1, __dmul_rn(dt, f1)), __dmul_rn(diffuse, acc1));
                 }
-                if (!interior<NDIM>(a.sh, q)) n0 = 0.0;
-                if (q + 1 >= a.n_m || !interior<NDIM>(a.sh, q + 1)) n1 = 0.0;
+                if (!in0) n0 = 0.0;
+                if (!in1) n1 = 0.0;
                 if (!live) break;
                 if (!isfinite(n0) || !isfinite(n1))
                     atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
@@ -1544,7 +1593,8 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
     }
     // one dense class holding every step (full / short memory): the dense kernel
     // streams it once for all steps; items would re-read it per 8 steps
-    if (ng == 1 && g[0].s == 1 && g[0].n == bt && bt > kItemCols) return false;
+    // (above kMaxDenseTBlock there is no dense kernel: items it is, each re-reading)
+    if (ng == 1 && g[0].s == 1 && g[0].n == bt && bt > kItemCols && p->tblock <= kMaxDenseTBlock) return false;
     int n = 0;
     int64_t crow = row0;
     for (int x = 0; x < ng; ++x) {

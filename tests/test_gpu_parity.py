@@ -410,7 +410,7 @@ def test_temporal_blocking_matches_goldens(fg, golden, name, tblock):
             assert err <= TOL, f"{name} tblock {tblock} member {b} step {s}: {err:.3e}"
 
 
-ADAPTIVE_SINGLE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_adaptive4"]
+ADAPTIVE_SINGLE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_adaptive4", "point_g05_adaptive1500"]
 
 
 @pytest.mark.parametrize("tblock", [48, 64])
