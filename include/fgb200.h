@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FGB200_ABI_VERSION 2
+#define FGB200_ABI_VERSION 3
 
 #define FG_OK 0
 #define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
@@ -92,7 +92,9 @@ typedef struct fg_plan {
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
     double* blkcoef_dev;         /* [2][coef_rows][36] scratch, single-member blocking:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */
-    double* Q_dev;               /* reserved, NULL                                   */
+    const double* psi_host;      /* optional, single member: host copy of psi_dev[0..tblock]
+                                    (blocked steps then get their coefficients as
+                                    launch parameters); NULL = read psi_dev       */
     int64_t q_rows;              /* reserved, 0                                      */
     int64_t coef_rows;           /* rows per blkcoef buffer (0 = h_slices)          */
 } fg_plan;

@@ -373,9 +373,15 @@ class Stepper:
                 # two blocks in flight; rows for the tail, every slice of the main
                 # launch and the slices two strides' items share
                 rows = 2 * (n + 1) + 4 * tb
+                if tb > 32:  # itemized only: a dense class is re-read by every 8-step item
+                    rows = (tb // 8 + 2) * (n + 1)
                 self.blkcoef = torch.empty((2, rows, _lib.FG_COEF_ROW), **f64)
                 plan.blkcoef_dev = self.blkcoef.data_ptr()
                 plan.coef_rows = rows
+                # host copy of ψ(0..tb): the library hands the blocked steps their
+                # coefficients as launch parameters (no ψ loads in the step chain)
+                self.psi_host = np.ascontiguousarray(self.psi[0, : tb + 1].cpu().numpy())
+                plan.psi_host = self.psi_host.ctypes.data
 
         self.tblock = int(plan.tblock)
         self.plan = plan

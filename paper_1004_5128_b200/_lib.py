@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FGB200_LIB") or os.path.join(HERE, "_lib", "libfgb200.so")
 
-ABI_VERSION = 2  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
+ABI_VERSION = 3  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
 FG_OK = 0
 FG_ERR_ARG = -1
 FG_ERR_CUDA = -2
@@ -73,7 +73,7 @@ class FgPlan(C.Structure):
         ("reserved2", C.c_int32),
         ("P_dev", C.c_void_p),
         ("blkcoef_dev", C.c_void_p),
-        ("Q_dev", C.c_void_p),
+        ("psi_host", C.c_void_p),
         ("q_rows", C.c_int64),
         ("coef_rows", C.c_int64),
     ]

@@ -86,6 +86,32 @@ __device__ __forceinline__ void st_pair(double* p, double a, double b) {
     *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
+// L2 eviction-priority hints.  The block stage streams the history through L2
+// (evict_first); what the latency-bound step chain reads next — the fields, the
+// newest history slices, the block's partial sums — is written evict_last so it
+// is still in L2 when read (misses would queue behind the stream in HBM).
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void st_pair_hint(double* p, double a, double b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ double2 ld_cg2_hint(const double* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -245,6 +271,12 @@ struct StepArgs {
     int32_t rw1;
     uint8_t rm[kMaxTBlock];
     uint8_t rwt[kMaxTBlock];
+    // single member with plan->psi_host: the coefficients themselves (w·ψ(m),
+    // rounded once on the host exactly like __dmul_rn), so the step kernel does
+    // no ψ loads and no conversions on its critical path
+    int32_t has_rc;
+    double rc0, rc1;
+    double rc[kMaxTBlock];
 };
 
 // Recent entries of step k in block kb0 (host and device): offsets 2 <= m <= bb
@@ -439,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
             __shared__ int32_t s_rn, s_w1;
             const uint8_t* rm = a.rm;
             const uint8_t* rwt = a.rwt;
+            const double* rcoef = a.has_rc ? a.rc : nullptr;
             int rn = a.rn;
             w1 = a.rw1;
             if (multi) {
@@ -446,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 __syncthreads();
                 rm = s_rm;
                 rwt = s_rwt;
+                rcoef = nullptr;
                 rn = s_rn;
                 w1 = s_w1;
             }
@@ -470,10 +504,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                         for (int u = 0; u < kR; ++u) {
                             const int e = e0 + u;
                             const int m = e < rn ? rm[e] : 0;
-                            const int w = (e < rn && m <= mmax) ? rwt[e] : 0;
-                            if (w) {
+                            const bool on = e < rn && m <= mmax;
+                            if (on) {
                                 v[u] = ld_stream(hbase - (int64_t)m * a.slice_stride);
-                                c[u] = __dmul_rn((double)w, __ldg(psi_b + m));
+                                c[u] = rcoef ? rcoef[e] : __dmul_rn((double)rwt[e], __ldg(psi_b + m));
                             } else {
                                 v[u] = make_double2(0.0, 0.0);
                                 c[u] = 0.0;
@@ -509,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
         const bool live = *(volatile const int64_t*)a.status > k;
 
         // ================= C: m = 1, m = 0, update =================
+        const uint64_t keep = l2_policy_last(), drop = l2_policy_first();
         const double* u_in = a.u[k & 1];
         double* u_out = a.u[(k + 1) & 1];
         double* snap = a.snap;
@@ -539,23 +574,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 } else {
                     d0 = delta_in<NDIM>(ub, a.sh, q, u0, in0);
                     d1 = delta_in<NDIM>(ub, a.sh, q + 1, u1, in1);
-                    if (live) st_pair(a.H + k * a.slice_stride + moff, d0, d1);
+                    if (live) st_pair_hint(a.H + k * a.slice_stride + moff, d0, d1, keep);
                 }
                 const double2 part = s_acc[p * kLanes + slot];
                 double acc0 = part.x, acc1 = part.y;
                 if (a.blocked) {  // slices t < kb0, summed by this block's fg_block_kernel
-                    const double2 pb = ld_cg2(a.P + bb * a.slice_stride + moff);
+                    const double2 pb = ld_cg2_hint(a.P + bb * a.slice_stride + moff, drop);  // its only read
                     acc0 = __dadd_rn(acc0, pb.x);
                     acc1 = __dadd_rn(acc1, pb.y);
                 }
                 const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
+                const bool host_c = BLK && a.has_rc && !multi;  // single-member coefficients from the host
                 if (has_m1 && len_b >= 2) {
-                    const double c1 = __dmul_rn((double)w1, __ldg(psi_b + 1));
+                    const double c1 = host_c ? a.rc1 : __dmul_rn((double)w1, __ldg(psi_b + 1));
                     const double2 h = ld_cg2(a.H + (k - 1) * a.slice_stride + moff);
                     acc0 = fma(c1, h.x, acc0);
                     acc1 = fma(c1, h.y, acc1);
                 }
-                const double c0 = __ldg(psi_b);  // w_0 * ψ(0) = 1 * 1
+                const double c0 = host_c ? a.rc0 : __ldg(psi_b);  // w_0 * ψ(0) = 1 * 1
                 acc0 = fma(c0, d0, acc0);
                 acc1 = fma(c0, d1, acc1);
 
@@ -578,8 +614,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 if (!live) break;
                 if (!isfinite(n0) || !isfinite(n1))
                     atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
-                st_pair(u_out + moff, n0, n1);
-                if (snap) st_pair(snap + moff, n0, n1);
+                st_pair_hint(u_out + moff, n0, n1, keep);
+                if (snap) st_pair_hint(snap + moff, n0, n1, drop);
             }
         }
         if (!live) return;  // uniform: every thread read the same flag
@@ -1127,6 +1163,7 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
             // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
             item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
         }
+        const uint64_t keep = l2_policy_last();  // the steps read P next
         // flush into P (this CTA owns the tile, items in table order, so the
         // sum of each step is deterministic): the first item of a step stores,
         // later ones (and every tail item) add — loads first, one round trip.
@@ -1150,9 +1187,9 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
                 const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
                 if (q >= a.n_m) continue;
                 if (add)
-                    st_pair(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]));
+                    st_pair_hint(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]), keep);
                 else
-                    st_pair(out + q, d[i][j][0], d[i][j][1]);
+                    st_pair_hint(out + q, d[i][j][0], d[i][j][1], keep);
             }
         }
     }
@@ -1397,6 +1434,12 @@ double* block_coef(const fg_plan* p, int64_t kb0) {
 // the schedule of step k (1 <= m <= k-kb0), for k in [k0, k1).
 void fill_recent(StepArgs& a, const fg_plan* p, int64_t kb0, int64_t k) {
     a.rn = recent_list(p->kind, k, kb0, p->base, a.hz_max, a.rm, a.rwt, &a.rw1);
+    if (p->psi_host && p->B == 1) {  // host doubles round like __dmul_rn (IEEE, no contraction)
+        a.has_rc = 1;
+        for (int e = 0; e < a.rn; ++e) a.rc[e] = (double)a.rwt[e] * p->psi_host[a.rm[e]];
+        a.rc1 = (double)a.rw1 * p->psi_host[1];
+        a.rc0 = p->psi_host[0];
+    }
 }
 
 // Ask for the largest shared-memory carveout for every kernel of the pipeline so
