@@ -64,16 +64,20 @@ def default_tblock(p: "Problem | None" = None) -> int:
 
     Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
     full memory at 32 (the dense block kernel turns fp64-tensor bound),
-    single-member adaptive at 48 (itemized block stage), short memory and
-    ensembles (per-member coefficient tables built in the CTA) at 24.
+    single-member adaptive at 48 and adaptive ensembles at 64 (itemized block
+    stage), short memory and other ensembles (per-member coefficient tables
+    built in the CTA) at 24.
     """
     env = os.environ.get("FGB200_TBLOCK")
     if env is not None:
         return int(env)
     if p is None:
         return 24
+    thinned = p.kind == "adaptive" and int(p.param) < int(p.n_steps)  # base >= n: the full schedule
     if p.batch > 1:
-        return 24
+        # ensembles: itemized (per-member coefficient rows) when thinned —
+        # c5 measured 3.7 s at 24, 2.09 s at 48, 1.81 s at 64; dense otherwise
+        return 64 if thinned else 24
     # a short memory at least as long as the run is the full schedule, and must
     # give the full schedule's bits (reference property, test_covering_strategies)
     truncating = p.kind == "short" and short_horizon(p.param, float(p.dt[0])) < int(p.n_steps)
@@ -81,7 +85,6 @@ def default_tblock(p: "Problem | None" = None) -> int:
         return 24
     # thinned schedules: the itemized block stage does work proportional to the
     # schedule's terms, so a wider block (fewer history passes) pays off
-    thinned = p.kind == "adaptive" and int(p.param) < int(p.n_steps)  # base >= n: the full schedule
     return 48 if thinned else 32
 
 
@@ -308,7 +311,16 @@ class Stepper:
         pool_slices = max(0, len([s for s in self.snap_steps if s > 0]))
         tb = default_tblock(p) if tblock is None else int(tblock)
         p_slices = 2 * tb if tb and n > tb else 0
+        ens_rows = 0
+        if tb and n > tb and B > 1 and p.kind == "adaptive":
+            # itemized ensembles: per-member item coefficient rows
+            # ([2][B][rows][36]; the shared schedule fixes the items, ψ_b the values)
+            need = C.c_int64(0)
+            _lib.check(L.fg_block_item_rows(_lib.MEM_KINDS["adaptive"], n, tb, int(p.param), 0, C.byref(need)),
+                       "fg_block_item_rows")
+            ens_rows = max(1, -(-need.value * _lib.FG_ITEM_PITCH // _lib.FG_COEF_ROW))
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
+        dev_bytes += 2 * B * ens_rows * _lib.FG_COEF_ROW * 8
         free, _total = torch.cuda.mem_get_info(self.device)
         free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
         if dev_bytes > free:
@@ -369,6 +381,10 @@ class Stepper:
             self.P = torch.empty((2, tb, slice_elems), **f64)
             plan.tblock = tb
             plan.P_dev = self.P.data_ptr()
+            if ens_rows:
+                self.blkcoef = torch.empty((2, B, ens_rows, _lib.FG_COEF_ROW), **f64)
+                plan.blkcoef_dev = self.blkcoef.data_ptr()
+                plan.coef_rows = ens_rows
             if B == 1:  # per-block coefficient rows shared by all tiles
                 # two blocks in flight; rows for the tail, every slice of the main
                 # launch and the slices two strides' items share

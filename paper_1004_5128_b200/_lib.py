@@ -24,6 +24,7 @@ FG_RUN_PERSISTENT = 4
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
+FG_ITEM_PITCH = 12  # doubles per item coefficient row (kItemPitch)
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
 REACTIONS = {"linear": 0, "saturating": 1}
@@ -32,7 +33,8 @@ REACTIONS = {"linear": 0, "saturating": 1}
 EXPORTS = (
     "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_kernel_launches", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
     "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_run_ex", "fg_status",
-    "fg_step_geometry", "fg_block_union", "fg_block_partials",
+    "fg_step_geometry", "fg_block_union", "fg_block_partials", "fg_block_item_rows",
+    "fg_block_item_table",
 )
 
 
@@ -105,6 +107,8 @@ def _declare(L):
         "fg_step_geometry": (C.c_int, [plan, _p64, _p32, _p32]),
         "fg_block_union": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
         "fg_block_partials": (C.c_int, [plan, i64, i32, vp]),
+        "fg_block_item_rows": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
+        "fg_block_item_table": (C.c_int, [i32, i64, i32, i64, i64, i64, i64, i32, _p64, i32, _p32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -646,7 +646,9 @@ struct BlockArgs {
     int32_t bt;
     int32_t n_m, kind, tpm, total_tiles;
     int32_t accumulate;      // P += D (tail launch) instead of P = D
-    const double* gcoef;  // single-member blocks: precomputed coefficient rows (or NULL)
+    const double* gcoef;  // precomputed coefficient rows (or NULL): single member, or
+                          // itemized ensembles ([B][coef_mstride] per block buffer)
+    int64_t coef_mstride; // doubles between members' coefficient rows (ensembles)
 };
 
 // The history rows are moved by the bulk-copy engine (cp.async.bulk → shared
@@ -1007,8 +1009,11 @@ struct ItemTable {
 // w·ψ(kb0 + col2step[c] - t_j) when that offset is in step col2step[c]'s
 // schedule with weight w == the item's stride (the entry belongs to this
 // item), else 0; columns ncols..CP-1 are zero padding for the DMMA tiles.
+// Ensembles (the schedule is shared, ψ is per member): blockIdx.z takes every
+// gridDim.z-th member; the entry's offset and weight are found once and reused
+// for each of its members' rows.
 __global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
-                                    double* __restrict__ out) {
+                                    double* __restrict__ out, int64_t n_members) {
     constexpr int CP = kItemPitch;
     __shared__ FgSeg segs[kItemCols][kBlkSegs];
     __shared__ int nseg[kItemCols];
@@ -1024,14 +1029,16 @@ __global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ I
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = e / CP;
         const int c = (int)(e - j * CP);
-        double v = 0.0;
+        int64_t m = -1;
+        int32_t w = 0;
         if (c < it.ncols) {
-            const int b = it.col2step[c];
-            const int64_t m = a.kb0 + b - (it.t_first + j * it.stride);
-            const int32_t w = fg_seg_weight(segs[c], nseg[c], m);
-            if (w == it.stride) v = __dmul_rn((double)w, __ldg(a.psi + m));
+            m = a.kb0 + it.col2step[c] - (it.t_first + j * it.stride);
+            w = fg_seg_weight(segs[c], nseg[c], m);
         }
-        out[((int64_t)it.coef_row + j) * CP + c] = v;
+        const bool on = w == it.stride;
+        double* o = out + ((int64_t)it.coef_row + j) * CP + c;
+        for (int64_t mem = blockIdx.z; mem < n_members; mem += gridDim.z)
+            o[mem * a.coef_mstride] = on ? __dmul_rn((double)w, __ldg(a.psi + mem * a.psi_stride + m)) : 0.0;
     }
 }
 
@@ -1074,7 +1081,9 @@ __device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double*
 // not drain between items): an item's slices are t_first + j*stride, DMMA M
 // tiles beyond its steps are skipped, and its partial sums are flushed from the
 // accumulators when its last stage is done.
-template <int TP, int NS>
+// ENS: ensembles (tpm tiles per member, per-member coefficient rows); the
+// single-member variant keeps the simpler addressing (and its registers).
+template <int TP, int NS, bool ENS>
 __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leave room for two step CTAs
     fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
     constexpr int kStages = NS;
@@ -1107,14 +1116,15 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
             const uint64_t pol = l2_evict_first_policy();
             int64_t g = 0;  // stage counter over all tiles and items
             for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-            const int64_t q0 = (int64_t)tile * TP;  // single member: tile = point range
-            const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+            const int64_t mem = ENS ? tile / a.tpm : 0;  // ensembles: tpm tiles per member
+            const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;
+            const int64_t row_elems = (a.ms - qm) < TP ? (a.ms - qm) : TP;
             const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
             for (int x = blockIdx.y; x < T.n_items; x += gridDim.y) {
                 const BlockItem& it = T.it[x];
-                const double* src0 = a.H + q0 + it.t_first * a.slice_stride;
+                const double* src0 = a.H + mem * a.ms + qm + it.t_first * a.slice_stride;
                 const int64_t sstride = (int64_t)it.stride * a.slice_stride;
-                const double* c0 = a.gcoef + (int64_t)it.coef_row * CP;
+                const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
                 for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
                     const int s = (int)(g % kStages);
                     if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
@@ -1136,13 +1146,15 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
     double d[MT][NT][2];
     int64_t g = 0;
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-    const int64_t q0 = (int64_t)tile * TP;
+    const int64_t mem = ENS ? tile / a.tpm : 0;
+    const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;  // tile's first point within its member
+    double* const Pm = ENS ? a.P + mem * a.ms : a.P;         // member's rows of P
     if (!T.accumulate) {  // steps no item adds to: P = 0 (this CTA owns the tile)
         for (uint64_t zm = T.zero_mask; zm; zm &= zm - 1) {
             const int b = __ffsll((long long)zm) - 1;
             for (int i = tid; i < TP / 2; i += TP) {
-                const int64_t q = q0 + 2 * i;
-                if (q < a.n_m) st_pair(a.P + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
+                const int64_t q = qm + 2 * i;
+                if (q < a.n_m) st_pair(Pm + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
             }
         }
     }
@@ -1174,17 +1186,17 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
         for (int i = 0; i < MT; ++i) {
             const int r = 8 * i + fr;
             if (i >= mt || r >= it.ncols) continue;
-            double* out = a.P + (int64_t)it.col2step[r] * a.slice_stride;
+            double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
             const bool add = T.accumulate || !((it.first_mask >> r) & 1);
             double2 old[NT];
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
+                const int64_t q = qm + warp * 32 + 8 * j + fk * 2;
                 old[j] = (add && q < a.n_m) ? ld_cg2(out + q) : make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
+                const int64_t q = qm + warp * 32 + 8 * j + fk * 2;
                 if (q >= a.n_m) continue;
                 if (add)
                     st_pair_hint(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]), keep);
@@ -1306,9 +1318,10 @@ int validate_plan(const fg_plan* p) {
     if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16 && p->tblock != 24 && p->tblock != 32 &&
         p->tblock != 48 && p->tblock != 64)
         return fail(FG_ERR_ARG, "tblock must be 0, 8, 16, 24, 32, 48 or 64");
-    if (p->tblock > kMaxDenseTBlock && (p->B != 1 || p->kind != FG_MEM_ADAPTIVE || !p->blkcoef_dev))
-        return fail(FG_ERR_UNSUPPORTED, "tblock %d needs a single-member adaptive plan with blkcoef_dev",
-                    (int)p->tblock);
+    if (p->tblock > kMaxDenseTBlock && (p->kind != FG_MEM_ADAPTIVE || !p->blkcoef_dev))
+        return fail(FG_ERR_UNSUPPORTED, "tblock %d needs an adaptive plan with blkcoef_dev", (int)p->tblock);
+    if (p->B > 1 && p->blkcoef_dev && p->kind != FG_MEM_ADAPTIVE)
+        return fail(FG_ERR_UNSUPPORTED, "ensemble coefficient rows (blkcoef_dev) are for adaptive plans only");
     if (p->tblock && !p->P_dev) return fail(FG_ERR_ARG, "temporal blocking needs P_dev");
     if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
         FgSeg s[FG_MAX_SEGS];
@@ -1426,8 +1439,9 @@ double* block_P(const fg_plan* p, int64_t kb0) {
 // launch can rebuild its rows while this block's tail launch still reads these.
 int64_t coef_capacity(const fg_plan* p) { return (p->coef_rows > 0 ? p->coef_rows : p->h_slices) * kCoefRow; }
 
+// Ensembles (itemized adaptive blocks): [2][B][capacity], member stride = capacity.
 double* block_coef(const fg_plan* p, int64_t kb0) {
-    return p->blkcoef_dev + ((kb0 / p->tblock) & 1) * coef_capacity(p);
+    return p->blkcoef_dev + ((kb0 / p->tblock) & 1) * p->B * coef_capacity(p);
 }
 
 // Recent-weight rows of a temporal block: a.rw[k-kb0][m] = weight of offset m in
@@ -1579,7 +1593,8 @@ BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& 
     a.kind = p->kind;
     a.tpm = (int32_t)((p->n_m + v.tp - 1) / v.tp);
     a.total_tiles = (int32_t)(a.tpm * p->B);
-    a.gcoef = (p->B == 1 && p->blkcoef_dev) ? block_coef(p, kb0) : nullptr;
+    a.gcoef = p->blkcoef_dev ? block_coef(p, kb0) : nullptr;
+    a.coef_mstride = coef_capacity(p);
     return a;
 }
 
@@ -1634,6 +1649,34 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
             if (g[x].n == 0 || g[x].cols[g[x].n - 1] != b) g[x].cols[g[x].n++] = (uint8_t)b;
         }
     }
+    // A class's groups must own disjoint slice ranges: the coefficient rows give
+    // an entry (step, t) to every item whose range holds t and whose columns hold
+    // the step, so two overlapping groups of one class would both add it.  A
+    // group can grow into another after both exist (adaptive tail-rule entries
+    // near t = 0 start a group that the dense window later reaches), so merge
+    // overlapping groups of a class (ranges and sorted column sets) to a fixpoint.
+    for (bool merged = true; merged;) {
+        merged = false;
+        for (int x = 0; x < ng && !merged; ++x)
+            for (int y = x + 1; y < ng && !merged; ++y) {
+                if (g[x].s != g[y].s || g[x].r != g[y].r || g[y].tmin > g[x].tmax || g[x].tmin > g[y].tmax) continue;
+                uint8_t cols[kMaxTBlock];
+                int n = 0, i = 0, j = 0;
+                while (i < g[x].n || j < g[y].n) {
+                    const int cx = i < g[x].n ? g[x].cols[i] : 1 << 30, cy = j < g[y].n ? g[y].cols[j] : 1 << 30;
+                    const int c = cx < cy ? cx : cy;
+                    cols[n++] = (uint8_t)c;
+                    i += cx == c;
+                    j += cy == c;
+                }
+                memcpy(g[x].cols, cols, (size_t)n);
+                g[x].n = n;
+                g[x].tmin = g[y].tmin < g[x].tmin ? g[y].tmin : g[x].tmin;
+                g[x].tmax = g[y].tmax > g[x].tmax ? g[y].tmax : g[x].tmax;
+                g[y] = g[--ng];
+                merged = true;
+            }
+    }
     // one dense class holding every step (full / short memory): the dense kernel
     // streams it once for all steps; items would re-read it per 8 steps
     // (above kMaxDenseTBlock there is no dense kernel: items it is, each re-reading)
@@ -1673,9 +1716,10 @@ int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
     int max_rows = 0;
     for (int x = 0; x < T.n_items; ++x) max_rows = T.it[x].n_slices > max_rows ? T.it[x].n_slices : max_rows;
     const int cx = (max_rows * kItemPitch + 255) / 256;
+    const int64_t B = a.total_tiles / a.tpm;
     ++g_launches;
-    fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items), 256, 0, st>>>(
-        a, T, const_cast<double*>(a.gcoef));
+    fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items, (unsigned)(B < 64 ? B : 64)),
+                          256, 0, st>>>(a, T, const_cast<double*>(a.gcoef), B);
     return cuda_check(cudaGetLastError(), "fg_item_coef launch");
 }
 
@@ -1685,24 +1729,30 @@ int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, i
                      bool tail = false) {
     void (*kern)(const BlockArgs, const ItemTable) = nullptr;
     size_t smem = 0;
+    const bool ens = p->B > 1;
+#define FG_ITEM_PICK(TPV)                                                                                          \
+    kern = tail ? (ens ? fg_block_item_kernel<TPV, kTailStages, true> : fg_block_item_kernel<TPV, kTailStages, false>) \
+                : (ens ? fg_block_item_kernel<TPV, kMainStages, true> : fg_block_item_kernel<TPV, kMainStages, false>); \
+    smem = tail ? item_block_smem<TPV, kTailStages>() : item_block_smem<TPV, kMainStages>();
     switch (tp) {
-        case 128: kern = tail ? fg_block_item_kernel<128, kTailStages> : fg_block_item_kernel<128, kMainStages>;
-                  smem = tail ? item_block_smem<128, kTailStages>() : item_block_smem<128, kMainStages>(); break;
-        case 192: kern = tail ? fg_block_item_kernel<192, kTailStages> : fg_block_item_kernel<192, kMainStages>;
-                  smem = tail ? item_block_smem<192, kTailStages>() : item_block_smem<192, kMainStages>(); break;
-        case 224: kern = tail ? fg_block_item_kernel<224, kTailStages> : fg_block_item_kernel<224, kMainStages>;
-                  smem = tail ? item_block_smem<224, kTailStages>() : item_block_smem<224, kMainStages>(); break;
-        default: kern = tail ? fg_block_item_kernel<256, kTailStages> : fg_block_item_kernel<256, kMainStages>;
-                 smem = tail ? item_block_smem<256, kTailStages>() : item_block_smem<256, kMainStages>(); tp = 256; break;
+        case 128: FG_ITEM_PICK(128) break;
+        case 192: FG_ITEM_PICK(192) break;
+        case 224: FG_ITEM_PICK(224) break;
+        default: FG_ITEM_PICK(256) tp = 256; break;
     }
+#undef FG_ITEM_PICK
     if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                             "item smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
-    // one CTA per tile (at most FGB200_BLOCK_CTAS_PER_SM per SM) walks all items:
-    // it owns the tile's P rows, so the items' adds need no atomics
+    // one CTA per tile (at most FGB200_BLOCK_CTAS_PER_SM per SM, looping over
+    // tiles — ensembles too) walks all items: it owns the tile's P rows, so the
+    // items' adds need no atomics
+    const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
+    const int per = e ? atoi(e) : 2;
+    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
     ++g_launches;
-    kern<<<block_grid(p, a.total_tiles), tp + 32, smem, st>>>(a, T);
+    kern<<<(unsigned)(a.total_tiles < cap ? a.total_tiles : cap), tp + 32, smem, st>>>(a, T);
     return cuda_check(cudaGetLastError(), "fg_block_item launch");
 }
 
@@ -1735,7 +1785,12 @@ bool items_enabled() {
 
 // Tail launches of factors above kMaxDenseTBlock are itemized too (the dense
 // kernel's accumulators would not fit).
-bool item_tail(const fg_plan* p) { return p->tblock > kMaxDenseTBlock; }
+// Itemized ensembles (blkcoef_dev given) itemize their tails as well; when a
+// tail does not fit the item table they fall back to the dense kernel, which
+// builds per-member coefficient tables in the CTA.
+bool item_tail(const fg_plan* p) {
+    return p->tblock > kMaxDenseTBlock || (p->B > 1 && p->blkcoef_dev && items_enabled());
+}
 
 int64_t tail_begin(const fg_plan* p, int64_t kb0) { return kb0 - p->tblock > 0 ? kb0 - p->tblock : 0; }
 
@@ -1755,36 +1810,42 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     a.t_begin = 0;
     a.t_end = tail_begin(p, kb0);
     if (a.gcoef) {
+        const bool ens = p->B > 1;  // ensembles: per-member item rows, no staged dense rows
         int64_t row0 = 0;  // main rows start after the tail's (in item-pitch rows when itemized)
         BlockArgs tail = a;
         tail.t_begin = tail_begin(p, kb0);
         tail.t_end = kb0;
         if (item_tail(p)) {
             ItemTable Tt;
-            if (!build_items(p, kb0, bt, tail.t_begin, tail.t_end, Tt, 0))
+            if (build_items(p, kb0, bt, tail.t_begin, tail.t_end, Tt, 0)) {
+                if (int rc = launch_item_coef(tail, Tt, st)) return rc;
+                for (int x = 0; x < Tt.n_items; ++x) row0 += Tt.it[x].n_slices;
+            } else if (!ens || p->tblock > kMaxDenseTBlock) {
                 return fail(FG_ERR_UNSUPPORTED, "tblock %d: tail of block %lld does not fit the item table",
                             (int)p->tblock, (long long)kb0);
-            if (int rc = launch_item_coef(tail, Tt, st)) return rc;
-            for (int x = 0; x < Tt.n_items; ++x) row0 += Tt.it[x].n_slices;
+            }  // else: the dense tail launch builds its own tables
         } else {
             if (int rc = launch_dense_coef(p, tail, st)) return rc;
             const int64_t cp = p->tblock + 4;
             row0 = (p->tblock * cp + kItemPitch - 1) / kItemPitch;  // dense tail rows, in item-pitch rows
         }
         ItemTable T;
-        const bool ok = items_enabled() || item_tail(p);
+        const bool ok = items_enabled() || p->tblock > kMaxDenseTBlock;
         if (ok && build_items(p, kb0, bt, 0, a.t_end, T, row0)) {
             if (T.n_items == 0)
-                return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->ms * sizeof(double), st),
-                                  "P reset");
+                return cuda_check(
+                    cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
+                    "P reset");
             if (int rc = launch_item_coef(a, T, st)) return rc;
             return launch_item_sums(p, a, T, v.tp, st);
         }
-        if (item_tail(p))
+        if (p->tblock > kMaxDenseTBlock)
             return fail(FG_ERR_UNSUPPORTED, "tblock %d: block %lld does not fit the item table", (int)p->tblock,
                         (long long)kb0);
-        a.gcoef += row0 * kItemPitch;
-        if (int rc = launch_dense_coef(p, a, st)) return rc;
+        if (!ens) {
+            a.gcoef += row0 * kItemPitch;
+            if (int rc = launch_dense_coef(p, a, st)) return rc;
+        }
     }
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
@@ -1807,12 +1868,14 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     a.accumulate = 1;
     if (item_tail(p)) {
         ItemTable T;
-        if (!build_items(p, kb0, bt, a.t_begin, a.t_end, T, 0))
+        if (build_items(p, kb0, bt, a.t_begin, a.t_end, T, 0)) {
+            if (T.n_items == 0) return FG_OK;
+            T.accumulate = 1;
+            return launch_item_sums(p, a, T, v.tp, st, true);
+        }
+        if (p->B == 1 || p->tblock > kMaxDenseTBlock)
             return fail(FG_ERR_UNSUPPORTED, "tblock %d: tail of block %lld does not fit the item table",
                         (int)p->tblock, (long long)kb0);
-        if (T.n_items == 0) return FG_OK;
-        T.accumulate = 1;
-        return launch_item_sums(p, a, T, v.tp, st, true);
     }
     if (int rc = cuda_check(cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem),
                             "block smem attribute"))
@@ -2282,6 +2345,71 @@ int fg_block_partials(const fg_plan* p, int64_t kb0, int32_t bt, void* stream) {
     if (kb0 < 0 || bt < 1 || bt > p->tblock || kb0 + bt > p->psi_stride || kb0 > p->h_slices)
         return fail(FG_ERR_ARG, "fg_block_partials: block out of range");
     return launch_block(p, kb0, bt, (cudaStream_t)stream);
+}
+
+int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t base, int64_t horizon,
+                       int64_t* max_rows) {
+    if (n_steps < 0 || tblock < 1 || tblock > kMaxTBlock || !max_rows)
+        return fail(FG_ERR_ARG, "fg_block_item_rows: bad arguments");
+    fg_plan q;
+    memset(&q, 0, sizeof q);
+    q.kind = kind;
+    q.base = base;
+    q.horizon_max = horizon;
+    q.tblock = tblock;
+    q.coef_rows = INT64_MAX / (4 * kCoefRow);  // no capacity limit while measuring
+    int64_t worst = 0;
+    static thread_local ItemTable T;
+    for (int64_t kb0 = tblock; kb0 < n_steps; kb0 += tblock) {
+        const int bt = (int)(n_steps - kb0 < tblock ? n_steps - kb0 : tblock);
+        const int64_t tb = kb0 - tblock;
+        int64_t rows = 0;
+        // a launch that does not itemize takes the dense kernel (no rows) when the
+        // factor has one, else the run fails — reported here already
+        if (build_items(&q, kb0, bt, tb, kb0, T, 0))
+            for (int x = 0; x < T.n_items; ++x) rows += T.it[x].n_slices;
+        else if (tblock > kMaxDenseTBlock)
+            return fail(FG_ERR_UNSUPPORTED, "tblock %d: tail of block %lld does not fit the item table", (int)tblock,
+                        (long long)kb0);
+        if (build_items(&q, kb0, bt, 0, tb, T, rows))
+            for (int x = 0; x < T.n_items; ++x) rows += T.it[x].n_slices;
+        else if (tblock > kMaxDenseTBlock)
+            return fail(FG_ERR_UNSUPPORTED, "tblock %d: block %lld does not fit the item table", (int)tblock,
+                        (long long)kb0);
+        worst = rows > worst ? rows : worst;
+    }
+    *max_rows = worst;
+    return FG_OK;
+}
+
+int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64_t te, int64_t base,
+                        int64_t horizon, int32_t tblock, int64_t* out, int32_t cap, int32_t* n_items) {
+    if (kb0 < 0 || bt < 1 || bt > kMaxTBlock || tblock < bt || tblock > kMaxTBlock || ts < 0 || te > kb0 || !out ||
+        !n_items)
+        return fail(FG_ERR_ARG, "fg_block_item_table: bad arguments");
+    fg_plan q;
+    memset(&q, 0, sizeof q);
+    q.kind = kind;
+    q.base = base;
+    q.horizon_max = horizon;
+    q.tblock = tblock;
+    q.coef_rows = INT64_MAX / (4 * kCoefRow);
+    static thread_local ItemTable T;
+    if (!build_items(&q, kb0, bt, ts, te, T, 0)) {
+        *n_items = -1;  // not itemized (dense class or table overflow)
+        return FG_OK;
+    }
+    *n_items = T.n_items;
+    if (T.n_items > cap) return fail(FG_ERR_ARG, "fg_block_item_table: %d items > cap %d", T.n_items, cap);
+    for (int x = 0; x < T.n_items; ++x) {
+        int64_t* o = out + (int64_t)x * 12;
+        o[0] = T.it[x].t_first;
+        o[1] = T.it[x].stride;
+        o[2] = T.it[x].n_slices;
+        o[3] = T.it[x].ncols;
+        for (int c = 0; c < kItemCols; ++c) o[4 + c] = c < T.it[x].ncols ? T.it[x].col2step[c] : -1;
+    }
+    return FG_OK;
 }
 
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count) {

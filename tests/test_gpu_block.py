@@ -39,7 +39,7 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
 
     tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64}.get(bt, 16)
     if tblock > 32 and kind != "adaptive":
-        pytest.skip("factors above 32 are single-member adaptive only")
+        pytest.skip("factors above 32 are adaptive only")
     n_steps = kb0 + bt + 1
     u0 = np.zeros(shape)
     strat = {"full": lambda: fg.FullMemory(), "short": lambda: fg.ShortMemory(param),
@@ -65,3 +65,41 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     got = P1[:, :n].cpu().numpy()
     scale = np.abs(want).max()
     assert np.abs(got - want).max() <= 1e-12 * max(scale, 1.0)
+
+
+@pytest.mark.parametrize("n_pts,B", [(300, 5), (512, 3), (40, 9)])
+@pytest.mark.parametrize("kb0,bt", [(16, 16), (160, 16), (1032, 24), (992, 32), (1008, 48), (1280, 64), (2000, 7)])
+def test_ensemble_block_partials_match_numpy(cuda_device, n_pts, B, kb0, bt):
+    """Itemized ensembles: the adaptive schedule is shared, each member has its
+    own ψ table (own γ) and its own coefficient rows; member rows are padded
+    (ms > n_m for 300 and 40 points)."""
+    import torch
+
+    import paper_1004_5128_b200 as fg
+    from paper_1004_5128_b200 import _lib
+    from paper_1004_5128_b200._engine import Stepper
+
+    tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64}.get(bt, 16)
+    n_steps = kb0 + bt + 1
+    gam = np.linspace(0.31, 0.89, B)
+    cfg = fg.FieldConfig(initial=np.zeros((B, n_pts)), dx=1.0, gamma=gam.tolist(), dt=[1.0] * B,
+                         n_steps=n_steps, strategy=fg.AdaptiveMemory(5), batched=True, history_byte_cap=None)
+    st = Stepper(cfg.to_problem(), tblock=tblock)
+    assert st.plan.blkcoef_dev, "ensemble adaptive plans carry per-member item coefficient rows"
+    gen = torch.Generator(device=st.device).manual_seed(kb0 * 3 + bt)
+    st.H.copy_(torch.randn(st.H.shape, generator=gen, device=st.device, dtype=torch.float64))
+    L = _lib.load()
+    _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
+    torch.cuda.synchronize()
+    P1 = st.block_partials(kb0)[:bt].clone()
+    _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
+    torch.cuda.synchronize()
+    assert torch.equal(P1, st.block_partials(kb0)[:bt]), "rerun differs"
+    ms = st.ms
+    Hs = st.H[:kb0].cpu().numpy().reshape(kb0, B, ms)
+    got = P1.cpu().numpy().reshape(bt, B, ms)
+    for b in range(B):
+        table = st.psi[b].cpu().numpy()
+        want = expected_partials(Hs[:, b, :n_pts], "adaptive", 5, kb0, bt, table)
+        scale = max(np.abs(want).max(), 1.0)
+        assert np.abs(got[:, b, :n_pts] - want).max() <= 1e-12 * scale, f"member {b}"

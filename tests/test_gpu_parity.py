@@ -410,13 +410,15 @@ def test_temporal_blocking_matches_goldens(fg, golden, name, tblock):
             assert err <= TOL, f"{name} tblock {tblock} member {b} step {s}: {err:.3e}"
 
 
-ADAPTIVE_SINGLE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_adaptive4", "point_g05_adaptive1500"]
+ADAPTIVE_WIDE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_adaptive4", "point_g05_adaptive1500",
+                 "batch_adaptive", "1d_adaptive", "3d_sat_adaptive"]
 
 
 @pytest.mark.parametrize("tblock", [48, 64])
-@pytest.mark.parametrize("name", ADAPTIVE_SINGLE)
+@pytest.mark.parametrize("name", ADAPTIVE_WIDE)
 def test_wide_temporal_blocking_matches_goldens(fg, golden, name, tblock):
-    """Factors above 32 (itemized main and tail launches, single-member adaptive)."""
+    """Factors above 32 (itemized main and tail launches; adaptive, single
+    member and ensembles with per-member ψ)."""
     test_temporal_blocking_matches_goldens(fg, golden, name, tblock)
 
 
