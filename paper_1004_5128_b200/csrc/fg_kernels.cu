@@ -1611,6 +1611,7 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
         int64_t s, r, tmin, tmax;
         int n;
         uint8_t cols[kMaxTBlock];
+        int64_t clo[kMaxTBlock], chi[kMaxTBlock];  // slice range of each column's entries in this group
     };
     static thread_local Grp g[kMaxItems];
     int ng = 0;
@@ -1646,7 +1647,15 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
                 g[x].tmin = t_lo < g[x].tmin ? t_lo : g[x].tmin;
                 g[x].tmax = t_hi > g[x].tmax ? t_hi : g[x].tmax;
             }
-            if (g[x].n == 0 || g[x].cols[g[x].n - 1] != b) g[x].cols[g[x].n++] = (uint8_t)b;
+            if (g[x].n == 0 || g[x].cols[g[x].n - 1] != b) {
+                g[x].clo[g[x].n] = t_lo;
+                g[x].chi[g[x].n] = t_hi;
+                g[x].cols[g[x].n++] = (uint8_t)b;
+            } else {
+                const int c = g[x].n - 1;
+                g[x].clo[c] = t_lo < g[x].clo[c] ? t_lo : g[x].clo[c];
+                g[x].chi[c] = t_hi > g[x].chi[c] ? t_hi : g[x].chi[c];
+            }
         }
     }
     // A class's groups must own disjoint slice ranges: the coefficient rows give
@@ -1661,15 +1670,28 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
             for (int y = x + 1; y < ng && !merged; ++y) {
                 if (g[x].s != g[y].s || g[x].r != g[y].r || g[y].tmin > g[x].tmax || g[x].tmin > g[y].tmax) continue;
                 uint8_t cols[kMaxTBlock];
+                int64_t lo[kMaxTBlock], hi[kMaxTBlock];
                 int n = 0, i = 0, j = 0;
                 while (i < g[x].n || j < g[y].n) {
                     const int cx = i < g[x].n ? g[x].cols[i] : 1 << 30, cy = j < g[y].n ? g[y].cols[j] : 1 << 30;
                     const int c = cx < cy ? cx : cy;
+                    lo[n] = INT64_MAX;
+                    hi[n] = INT64_MIN;
+                    if (cx == c) {
+                        lo[n] = g[x].clo[i];
+                        hi[n] = g[x].chi[i];
+                        ++i;
+                    }
+                    if (cy == c) {
+                        lo[n] = g[y].clo[j] < lo[n] ? g[y].clo[j] : lo[n];
+                        hi[n] = g[y].chi[j] > hi[n] ? g[y].chi[j] : hi[n];
+                        ++j;
+                    }
                     cols[n++] = (uint8_t)c;
-                    i += cx == c;
-                    j += cy == c;
                 }
                 memcpy(g[x].cols, cols, (size_t)n);
+                memcpy(g[x].clo, lo, sizeof(int64_t) * n);
+                memcpy(g[x].chi, hi, sizeof(int64_t) * n);
                 g[x].n = n;
                 g[x].tmin = g[y].tmin < g[x].tmin ? g[y].tmin : g[x].tmin;
                 g[x].tmax = g[y].tmax > g[x].tmax ? g[y].tmax : g[x].tmax;
@@ -1687,11 +1709,18 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
         for (int c0 = 0; c0 < g[x].n; c0 += kItemCols) {
             if (n == kMaxItems) return false;
             BlockItem& it = T.it[n++];
-            it.t_first = g[x].tmin;
             it.stride = (int32_t)g[x].s;
-            it.n_slices = (int32_t)((g[x].tmax - g[x].tmin) / g[x].s + 1);
             it.ncols = g[x].n - c0 < kItemCols ? g[x].n - c0 : kItemCols;
-            for (int c = 0; c < it.ncols; ++c) it.col2step[c] = g[x].cols[c0 + c];
+            // the item streams only the slices its own steps use (an 8-step item of
+            // a dense class spans its steps' windows, not the whole group)
+            int64_t lo = INT64_MAX, hi = INT64_MIN;
+            for (int c = 0; c < it.ncols; ++c) {
+                it.col2step[c] = g[x].cols[c0 + c];
+                lo = g[x].clo[c0 + c] < lo ? g[x].clo[c0 + c] : lo;
+                hi = g[x].chi[c0 + c] > hi ? g[x].chi[c0 + c] : hi;
+            }
+            it.t_first = lo;
+            it.n_slices = (int32_t)((hi - lo) / g[x].s + 1);
             it.coef_row = (int32_t)crow;
             crow += it.n_slices;
         }
