@@ -86,7 +86,8 @@ typedef struct fg_plan {
                                     (filled by fg_run; NULL if no snapshots)       */
     int64_t horizon_max;         /* host copy of max(horizon_dev) (0 = unknown)    */
     int32_t tblock;              /* temporal blocking factor: 0 (off), 8, 16, 24, 32;
-                                    48 / 64 for single-member adaptive plans only  */
+                                    multiples of 8 up to 128 above 32 for adaptive
+                                    plans (itemized block stage, blkcoef_dev)     */
     int32_t reserved2;
     double* P_dev;               /* [2][tblock][B*ms] scratch for blocked partial sums:
                                     block kb0 uses buffer (kb0 / tblock) & 1        */

@@ -64,9 +64,8 @@ def default_tblock(p: "Problem | None" = None) -> int:
 
     Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
     full memory at 32 (the dense block kernel turns fp64-tensor bound),
-    single-member adaptive at 48 and adaptive ensembles at 64 (itemized block
-    stage), short memory and other ensembles (per-member coefficient tables
-    built in the CTA) at 24.
+    adaptive at 64, single member and ensembles (itemized block stage), short
+    memory and other ensembles (per-member tables built in the CTA) at 24.
     """
     env = os.environ.get("FGB200_TBLOCK")
     if env is not None:
@@ -84,8 +83,10 @@ def default_tblock(p: "Problem | None" = None) -> int:
     if truncating:
         return 24
     # thinned schedules: the itemized block stage does work proportional to the
-    # schedule's terms, so a wider block (fewer history passes) pays off
-    return 48 if thinned else 32
+    # schedule's terms, so a wider block (fewer history passes) pays off up to
+    # 64 (c2: 31.7 ms at 48, 30.2 at 64, 33.9 at 80, 36.2 at 128 — wider blocks
+    # re-read classes with more than 8 steps and lengthen the step chain)
+    return 64 if thinned else 32
 
 
 def round_up(n: int, m: int) -> int:

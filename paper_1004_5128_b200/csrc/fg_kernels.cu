@@ -64,9 +64,9 @@ constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit loa
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
-constexpr int kMaxTBlock = 64;  // largest temporal-blocking factor (> 32: itemized stages only)
+constexpr int kMaxTBlock = 128;  // largest temporal-blocking factor (> 32: itemized stages only)
 constexpr int kMaxDenseTBlock = 32;  // largest factor of the dense block kernel
-constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxTBlock + 4)
+constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxDenseTBlock + 4)
 
 // ---------------------------------------------------------------- PTX helpers ---
 
@@ -1001,7 +1001,7 @@ struct BlockItem {
 struct ItemTable {
     int32_t n_items;
     int32_t accumulate;  // tail launch: every item adds to P (no first stores, no zeroing)
-    uint64_t zero_mask;  // main launch: steps no item touches (their P rows are zeroed)
+    uint64_t zero_mask[kMaxTBlock / 64];  // main launch: steps no item touches (their P rows are zeroed)
     BlockItem it[kMaxItems];
 };
 
@@ -1150,8 +1150,9 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
     const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;  // tile's first point within its member
     double* const Pm = ENS ? a.P + mem * a.ms : a.P;         // member's rows of P
     if (!T.accumulate) {  // steps no item adds to: P = 0 (this CTA owns the tile)
-        for (uint64_t zm = T.zero_mask; zm; zm &= zm - 1) {
-            const int b = __ffsll((long long)zm) - 1;
+        for (int w = 0; w < kMaxTBlock / 64; ++w)
+        for (uint64_t zm = T.zero_mask[w]; zm; zm &= zm - 1) {
+            const int b = 64 * w + __ffsll((long long)zm) - 1;
             for (int i = tid; i < TP / 2; i += TP) {
                 const int64_t q = qm + 2 * i;
                 if (q < a.n_m) st_pair(Pm + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
@@ -1315,9 +1316,9 @@ int validate_plan(const fg_plan* p) {
         return fail(FG_ERR_ARG, "plan has a NULL device pointer");
     if (p->split != 0 && p->split != 1 && p->split != 2 && p->split != 4 && p->split != 8)
         return fail(FG_ERR_ARG, "split must be 0, 1, 2, 4 or 8");
-    if (p->tblock != 0 && p->tblock != 8 && p->tblock != 16 && p->tblock != 24 && p->tblock != 32 &&
-        p->tblock != 48 && p->tblock != 64)
-        return fail(FG_ERR_ARG, "tblock must be 0, 8, 16, 24, 32, 48 or 64");
+    if (p->tblock < 0 || p->tblock > kMaxTBlock || p->tblock % 8 != 0 ||
+        (p->tblock > 0 && p->tblock < 32 && p->tblock != 8 && p->tblock != 16 && p->tblock != 24))
+        return fail(FG_ERR_ARG, "tblock must be 0, 8, 16, 24 or a multiple of 8 from 32 to %d", kMaxTBlock);
     if (p->tblock > kMaxDenseTBlock && (p->kind != FG_MEM_ADAPTIVE || !p->blkcoef_dev))
         return fail(FG_ERR_UNSUPPORTED, "tblock %d needs an adaptive plan with blkcoef_dev", (int)p->tblock);
     if (p->B > 1 && p->blkcoef_dev && p->kind != FG_MEM_ADAPTIVE)
@@ -1726,16 +1727,20 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
         }
     }
     T.n_items = n;
-    uint64_t seen = 0;
+    uint64_t seen[kMaxTBlock / 64] = {};
     for (int x = 0; x < n; ++x) {
         BlockItem& it = T.it[x];
         for (int c = 0; c < it.ncols; ++c) {
-            const uint64_t bit = 1ull << it.col2step[c];
-            if (!(seen & bit)) it.first_mask |= 1 << c;
-            seen |= bit;
+            const int w = it.col2step[c] >> 6;
+            const uint64_t bit = 1ull << (it.col2step[c] & 63);
+            if (!(seen[w] & bit)) it.first_mask |= 1 << c;
+            seen[w] |= bit;
         }
     }
-    T.zero_mask = ~seen & (bt >= 64 ? ~0ull : ((1ull << bt) - 1));
+    for (int w = 0; w < kMaxTBlock / 64; ++w) {
+        const int nb = bt - 64 * w;  // steps of the block in this word
+        T.zero_mask[w] = ~seen[w] & (nb >= 64 ? ~0ull : nb <= 0 ? 0ull : ((1ull << nb) - 1));
+    }
     if (crow * kItemPitch > coef_capacity(p)) return false;
     return true;
 }
@@ -2442,7 +2447,7 @@ int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64
 }
 
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count) {
-    if (kb0 < 0 || bt < 1 || bt > 64 || !count) return fail(FG_ERR_ARG, "fg_block_union: bad arguments");
+    if (kb0 < 0 || bt < 1 || bt > kMaxTBlock || !count) return fail(FG_ERR_ARG, "fg_block_union: bad arguments");
     std::vector<char> used((size_t)kb0, 0);
     FgSeg s[FG_MAX_SEGS];
     for (int b = 0; b < bt; ++b) {

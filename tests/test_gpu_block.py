@@ -29,7 +29,7 @@ def expected_partials(H, kind, param, kb0, bt, table, dt=1.0):
     ((256, 256), "adaptive", 5), ((256, 256), "full", 0), ((48, 48), "adaptive", 3), ((4096,), "full", 0),
     ((300,), "adaptive", 2), ((64, 64), "short", 37.0)])
 @pytest.mark.parametrize("kb0,bt", [(16, 16), (160, 16), (1030, 16), (2000, 7), (517, 8), (48, 24), (1200, 24),
-                                    (999, 32), (64, 64), (1280, 64), (1000, 48)])
+                                    (999, 32), (64, 64), (1280, 64), (1000, 48), (1920, 96), (2048, 128)])
 def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     import torch
 
@@ -37,7 +37,7 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     from paper_1004_5128_b200 import _lib
     from paper_1004_5128_b200._engine import Stepper
 
-    tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64}.get(bt, 16)
+    tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64, 96: 96, 128: 128}.get(bt, 16)
     if tblock > 32 and kind != "adaptive":
         pytest.skip("factors above 32 are adaptive only")
     n_steps = kb0 + bt + 1
@@ -68,7 +68,7 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
 
 
 @pytest.mark.parametrize("n_pts,B", [(300, 5), (512, 3), (40, 9)])
-@pytest.mark.parametrize("kb0,bt", [(16, 16), (160, 16), (1032, 24), (992, 32), (1008, 48), (1280, 64), (2000, 7)])
+@pytest.mark.parametrize("kb0,bt", [(16, 16), (160, 16), (1032, 24), (992, 32), (1008, 48), (1280, 64), (2000, 7), (1920, 128)])
 def test_ensemble_block_partials_match_numpy(cuda_device, n_pts, B, kb0, bt):
     """Itemized ensembles: the adaptive schedule is shared, each member has its
     own ψ table (own γ) and its own coefficient rows; member rows are padded
@@ -79,7 +79,7 @@ def test_ensemble_block_partials_match_numpy(cuda_device, n_pts, B, kb0, bt):
     from paper_1004_5128_b200 import _lib
     from paper_1004_5128_b200._engine import Stepper
 
-    tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64}.get(bt, 16)
+    tblock = {8: 8, 24: 24, 32: 32, 48: 48, 64: 64, 96: 96, 128: 128}.get(bt, 16)
     n_steps = kb0 + bt + 1
     gam = np.linspace(0.31, 0.89, B)
     cfg = fg.FieldConfig(initial=np.zeros((B, n_pts)), dx=1.0, gamma=gam.tolist(), dt=[1.0] * B,

@@ -65,7 +65,7 @@ def check_ownership(kb0, bt, ts, te, base, tblock):
 
 
 @pytest.mark.parametrize("base", [2, 3, 5, 8])
-@pytest.mark.parametrize("tblock", [8, 16, 24, 32, 48, 64])
+@pytest.mark.parametrize("tblock", [8, 16, 24, 32, 48, 64, 80, 128])
 def test_every_entry_owned_once(base, tblock):
     """Tails ([kb0 - tblock, kb0)) and main ranges ([0, kb0 - tblock)) of the
     first blocks (where the adaptive tail rule and the dense window share a
