@@ -170,6 +170,11 @@ int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
 #define FG_RUN_GRAPH 1
 #define FG_RUN_PDL 2
 #define FG_RUN_PERSISTENT 4
+/* Temporal blocking: one launch per block whose CTAs (one per tile) wait only
+ * for the tiles their stencil reads, one step apart (no grid barrier, no
+ * per-step launch); used when every tile's CTA fits on the GPU at once, else
+ * per-step launches.  Results are bitwise identical to the other modes. */
+#define FG_RUN_CHAIN 32
 /* Temporal blocking: P_dev already holds the partial sums of the block that
  * contains k0 (this call continues the previous fg_run of the same plan), so a
  * block that started before k0 is not recomputed. */

@@ -21,6 +21,7 @@ FG_NO_BAD_STEP = (1 << 63) - 1
 FG_RUN_GRAPH = 1
 FG_RUN_PDL = 2
 FG_RUN_PERSISTENT = 4
+FG_RUN_CHAIN = 32
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
