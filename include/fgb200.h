@@ -81,7 +81,8 @@ typedef struct fg_plan {
     int64_t* status_dev;         /* [2]: [0] first non-finite step or FG_NO_BAD_STEP,
                                     [1] grid-barrier counter (library scratch)     */
     int32_t step_flags;          /* FG_STEP_* bits                                 */
-    int32_t reserved;
+    int32_t item_cols;           /* itemized block stage: step columns per item, 8 or 16
+                                    (0 = FGB200_ITEM_COLS, else 16 for ensembles, 8 otherwise) */
     int32_t* snap_slot_dev;      /* [h_slices+1] scratch for FG_RUN_PERSISTENT snapshots
                                     (filled by fg_run; NULL if no snapshots)       */
     int64_t horizon_max;         /* host copy of max(horizon_dev) (0 = unknown)    */
@@ -199,18 +200,20 @@ int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);
  * t < kb0 that the block of steps kb0..kb0+bt-1 reads (the union of their
  * schedules' old parts), i.e. the slices fg_block_kernel streams once. */
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count);
-/* Largest number of item coefficient rows (tail + main, 12 doubles each) any
- * temporal block of an n_steps run needs: sizes blkcoef_dev for itemized
- * ensembles (coef_rows >= ceil(rows * 12 / 36)).  Host-only, no device work. */
+/* Largest number of item coefficient rows (tail + main; 12 doubles each for
+ * 8-column items, 20 for 16-column items) any temporal block of an n_steps run
+ * needs: sizes blkcoef_dev for itemized ensembles (coef_rows >= ceil(rows *
+ * pitch / 36)).  Host-only, no device work. */
 /* Host-only view of the item table the library builds for a temporal block
- * (steps kb0..kb0+bt-1, old slices [ts, te)): 12 int64 per item = t_first,
- * stride, n_slices, ncols, the ncols step columns (padded with -1).  *n_items =
+ * (steps kb0..kb0+bt-1, old slices [ts, te)): 20 int64 per item = t_first,
+ * stride, n_slices, ncols, the ncols (<= 16) step columns (padded with -1).  *n_items =
  * -1 when the range is not itemized (one dense class, or the table overflows).
  * Lets tests prove every schedule entry is owned by exactly one item. */
 int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64_t te, int64_t base,
-                        int64_t horizon, int32_t tblock, int64_t* out, int32_t cap, int32_t* n_items);
+                        int64_t horizon, int32_t tblock, int32_t item_cols, int64_t* out, int32_t cap,
+                        int32_t* n_items);
 int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t base, int64_t horizon,
-                       int64_t* max_rows);
+                       int32_t item_cols, int64_t* max_rows);
 
 /* Temporal blocking building block (normally driven by fg_run): write into
  * buffer (kb0 / tblock) & 1 of plan->P_dev the partial sums of steps

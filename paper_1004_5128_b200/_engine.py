@@ -63,9 +63,10 @@ def default_tblock(p: "Problem | None" = None) -> int:
     """Temporal blocking factor (0 = off): one history pass feeds this many steps.
 
     Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
-    full memory at 32 (the dense block kernel turns fp64-tensor bound),
-    adaptive at 64, single member and ensembles (itemized block stage), short
-    memory and other ensembles (per-member tables built in the CTA) at 24.
+    full memory at 32 (the dense block kernel turns fp64-tensor bound);
+    adaptive at 128 with 16-column items for large fields (c3, c4, c5) and at
+    64 with 8-column items otherwise (c2); short memory and other ensembles
+    (per-member tables built in the CTA) at 24.
     """
     env = os.environ.get("FGB200_TBLOCK")
     if env is not None:
@@ -73,9 +74,11 @@ def default_tblock(p: "Problem | None" = None) -> int:
     if p is None:
         return 24
     thinned = p.kind == "adaptive" and int(p.param) < int(p.n_steps)  # base >= n: the full schedule
+    if thinned and large_field(p):
+        # 16-column items (see item_cols): one history pass per 128 steps
+        return 128
     if p.batch > 1:
-        # ensembles: itemized (per-member coefficient rows) when thinned —
-        # c5 measured 3.7 s at 24, 2.09 s at 48, 1.81 s at 64; dense otherwise
+        # ensembles: itemized (per-member coefficient rows) when thinned; dense otherwise
         return 64 if thinned else 24
     # a short memory at least as long as the run is the full schedule, and must
     # give the full schedule's bits (reference property, test_covering_strategies)
@@ -87,6 +90,27 @@ def default_tblock(p: "Problem | None" = None) -> int:
     # 64 (c2: 31.7 ms at 48, 30.2 at 64, 33.9 at 80, 36.2 at 128 — wider blocks
     # re-read classes with more than 8 steps and lengthen the step chain)
     return 64 if thinned else 32
+
+
+def item_cols(p: "Problem") -> int:
+    """Step columns per item of the itemized block stage (fg_plan.item_cols).
+
+    16-column items stream a residue class of up to 16 steps once (narrow
+    tiles); 8-column items use wider tiles.  Measured on B200 (ms per run):
+    c2 8/64 30.2, 16/128 37.8; c3-adaptive 8/64 352, 16/128 336; c4-adaptive
+    8/64 716, 16/128 687; c5 8/64 1780, 16/128 1400.  FGB200_ITEM_COLS overrides.
+    """
+    env = os.environ.get("FGB200_ITEM_COLS")
+    if env in ("8", "16"):
+        return int(env)
+    return 16 if large_field(p) else 8
+
+
+def large_field(p: "Problem") -> bool:
+    """Fields of >= 2^19 points in all (c3, c4, c5): their step chain keeps up
+    with a block stage at tblock 128 and 16-column items; smaller ones (c2)
+    are step-chain bound and run best at tblock 64 with 8-column items."""
+    return p.batch * p.n_m >= 1 << 19
 
 
 def round_up(n: int, m: int) -> int:
@@ -317,9 +341,10 @@ class Stepper:
             # itemized ensembles: per-member item coefficient rows
             # ([2][B][rows][36]; the shared schedule fixes the items, ψ_b the values)
             need = C.c_int64(0)
-            _lib.check(L.fg_block_item_rows(_lib.MEM_KINDS["adaptive"], n, tb, int(p.param), 0, C.byref(need)),
-                       "fg_block_item_rows")
-            ens_rows = max(1, -(-need.value * _lib.FG_ITEM_PITCH // _lib.FG_COEF_ROW))
+            icols = item_cols(p)
+            _lib.check(L.fg_block_item_rows(_lib.MEM_KINDS["adaptive"], n, tb, int(p.param), 0, icols,
+                                            C.byref(need)), "fg_block_item_rows")
+            ens_rows = max(1, -(-need.value * _lib.FG_ITEM_PITCH[icols] // _lib.FG_COEF_ROW))
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         dev_bytes += 2 * B * ens_rows * _lib.FG_COEF_ROW * 8
         free, _total = torch.cuda.mem_get_info(self.device)
@@ -375,6 +400,7 @@ class Stepper:
         plan.status_dev = self.status.data_ptr()
         plan.snap_slot_dev = self.snap_slot.data_ptr() if self.snap_slot is not None else None
         plan.horizon_max = max(hz) if p.kind == "short" else 0
+        plan.item_cols = item_cols(p)
         self.P = None
         if tb and n > tb:
             # two buffers: block j's steps read one while block j+1's main launch

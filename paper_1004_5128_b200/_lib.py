@@ -25,7 +25,7 @@ FG_RUN_CHAIN = 32
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
-FG_ITEM_PITCH = 12  # doubles per item coefficient row (kItemPitch)
+FG_ITEM_PITCH = {8: 12, 16: 20}  # doubles per item coefficient row by item width (kItemPitch8 / kItemPitch)
 
 MEM_KINDS = {"full": 0, "short": 1, "adaptive": 2}
 REACTIONS = {"linear": 0, "saturating": 1}
@@ -69,7 +69,7 @@ class FgPlan(C.Structure):
         ("u_dev", C.c_void_p * 2),
         ("status_dev", C.c_void_p),
         ("step_flags", C.c_int32),
-        ("reserved", C.c_int32),
+        ("item_cols", C.c_int32),
         ("snap_slot_dev", C.c_void_p),
         ("horizon_max", C.c_int64),
         ("tblock", C.c_int32),
@@ -108,8 +108,8 @@ def _declare(L):
         "fg_step_geometry": (C.c_int, [plan, _p64, _p32, _p32]),
         "fg_block_union": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
         "fg_block_partials": (C.c_int, [plan, i64, i32, vp]),
-        "fg_block_item_rows": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
-        "fg_block_item_table": (C.c_int, [i32, i64, i32, i64, i64, i64, i64, i32, _p64, i32, _p32]),
+        "fg_block_item_rows": (C.c_int, [i32, i64, i32, i64, i64, i32, _p64]),
+        "fg_block_item_table": (C.c_int, [i32, i64, i32, i64, i64, i64, i64, i32, i32, _p64, i32, _p32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1121,9 +1121,11 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 // and short memory (one class holding every step) keep the dense kernel.
 
 constexpr int kMaxItems = 160;
-constexpr int kItemCols = 8;    // steps per item: one DMMA M tile, so the kernel's
+constexpr int kItemCols = 16;   // steps per item: two DMMA M tiles, so the kernel's
                                 // accumulators (and registers) do not grow with tblock
-constexpr int kItemPitch = kItemCols + 4;  // coefficient row pitch (conflict-free, see coef_pitch)
+constexpr int kItemPitch = kItemCols + 4;  // coefficient row pitch: 20 ≡ 4 (mod 16) doubles, conflict-free
+                                           // A-fragment loads (see coef_pitch)
+constexpr int kItemPitch8 = 12;            // 8-column items (fg_block_item8_kernel): 12 ≡ -4 (mod 16)
 
 struct BlockItem {
     int64_t t_first;
@@ -1137,6 +1139,8 @@ struct BlockItem {
 struct ItemTable {
     int32_t n_items;
     int32_t accumulate;  // tail launch: every item adds to P (no first stores, no zeroing)
+    int32_t cols;        // item width of this table: 8 (fg_block_item8_kernel) or 16
+    int32_t pitch;       // its coefficient row pitch: kItemPitch8 or kItemPitch
     uint64_t zero_mask[kMaxTBlock / 64];  // main launch: steps no item touches (their P rows are zeroed)
     BlockItem it[kMaxItems];
 };
@@ -1150,7 +1154,7 @@ struct ItemTable {
 // for each of its members' rows.
 __global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
                                     double* __restrict__ out, int64_t n_members) {
-    constexpr int CP = kItemPitch;
+    const int CP = T.pitch;
     __shared__ FgSeg segs[kItemCols][kBlkSegs];
     __shared__ int nseg[kItemCols];
     const BlockItem& it = T.it[blockIdx.y];
@@ -1212,6 +1216,11 @@ __device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double*
             for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
 }
 
+// ---- 8-column items (fg_block_item8_kernel): warps of 32 points, one DMMA M
+// tile.  Wider tiles per CTA (TP 128..256) than the 16-column kernel below, so a
+// CTA walks the item table fewer times: measured faster for a single small
+// field (c2: 22.9 vs 31.9 ms of block stage at tblock 64), while 16-column items
+// win when a class has more than 8 steps in a block (c5 at tblock 128).
 // One CTA per tile walks every item in table order through one TMA ring (the
 // ring of fg_block_tma_kernel with staged coefficient rows; the pipeline does
 // not drain between items): an item's slices are t_first + j*stride, DMMA M
@@ -1221,10 +1230,10 @@ __device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double*
 // single-member variant keeps the simpler addressing (and its registers).
 template <int TP, int NS, bool ENS>
 __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leave room for two step CTAs
-    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
+    fg_block_item8_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
     constexpr int kStages = NS;
     constexpr int RP = row_pitch<TP>();
-    constexpr int CP = kItemPitch;
+    constexpr int CP = kItemPitch8;
     constexpr int MT = 1;
     constexpr int NT = 4;
     constexpr int NW = TP / 32;
@@ -1346,9 +1355,163 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
 }
 
 template <int TP, int NS>
+size_t item8_block_smem() {
+    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * kItemPitch8 * sizeof(double) +
+           (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
+}
+
+// One CTA per SM walks its tiles, and per tile every item in table order,
+// through one TMA ring (the ring of fg_block_tma_kernel with staged coefficient
+// rows; the pipeline does not drain between items or tiles): an item's slices
+// are t_first + j*stride, and its partial sums are flushed from the
+// accumulators when its last stage is done.  An item has up to 16 step columns
+// (two DMMA M tiles), so a residue class of up to 16 steps is streamed once; a
+// warp owns 16 points of the tile (two N tiles), which keeps the accumulators
+// at 8 doubles per thread — TP/16 consumer warps + 1 producer warp, <= 64
+// registers, two CTAs per SM (measured: one CTA of 14 warps per SM streamed at
+// half the rate, its item flushes stalling the SM's only ring), and two step
+// CTAs still fit beside them.  Items of at most 8 columns issue only the first
+// M tile (warp-uniform branch).
+// ENS: ensembles (tpm tiles per member, per-member coefficient rows); the
+// single-member variant keeps the simpler addressing.
+template <int TP>
+constexpr int item_threads() { return TP / 16 * 32 + 32; }
+
+template <int TP, int NS, bool ENS>
+__global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside two of these per SM
+    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
+    constexpr int kStages = NS;
+    constexpr int RP = row_pitch<TP>();
+    constexpr int CP = kItemPitch;
+    constexpr int MT = 2;
+    constexpr int NT = 2;
+    constexpr int NW = TP / 16;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* rows = reinterpret_cast<double*>(smem);                        // [kStages][kE][RP]
+    double* coef = rows + kStages * kE * RP;                              // [kStages*kE][CP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kE * CP);
+    uint64_t* empty = full + kStages;
+    double* sink = reinterpret_cast<double*>(empty + kStages);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NW) {  // producer warp: lane e < nr issues row e of a stage, lane kE its coefficients
+        const uint64_t pol = l2_evict_first_policy();
+        int64_t g = 0;  // stage counter over all tiles and items
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            const int64_t mem = ENS ? tile / a.tpm : 0;  // ensembles: tpm tiles per member
+            const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;
+            const int64_t row_elems = (a.ms - qm) < TP ? (a.ms - qm) : TP;
+            const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+            for (int x = 0; x < T.n_items; ++x) {
+                const BlockItem& it = T.it[x];
+                const double* src0 = a.H + mem * a.ms + qm + it.t_first * a.slice_stride;
+                const int64_t sstride = (int64_t)it.stride * a.slice_stride;
+                const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
+                for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+                    const int s = (int)(g % kStages);
+                    const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
+                    if (lane == 0) {
+                        if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
+                        mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + (uint32_t)(nr * CP * sizeof(double)));
+                    }
+                    __syncwarp();
+                    if (lane < nr)
+                        bulk_g2s_hint(rows + ((size_t)s * kE + lane) * RP, src0 + (j0 + lane) * sstride, row_bytes,
+                                      &full[s], pol);
+                    else if (lane == kE)
+                        bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, (uint32_t)(nr * CP * sizeof(double)),
+                                 &full[s]);
+                }
+            }
+        }  // tiles
+        return;
+    }
+
+    const int fr = lane >> 2, fk = lane & 3;
+    double d[MT][NT][2];
+    int64_t g = 0;
+    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    const int64_t mem = ENS ? tile / a.tpm : 0;
+    const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;  // tile's first point within its member
+    double* const Pm = ENS ? a.P + mem * a.ms : a.P;         // member's rows of P
+    if (!T.accumulate) {  // steps no item adds to: P = 0 (this CTA owns the tile)
+        for (int w = 0; w < kMaxTBlock / 64; ++w)
+        for (uint64_t zm = T.zero_mask[w]; zm; zm &= zm - 1) {
+            const int b = 64 * w + __ffsll((long long)zm) - 1;
+            for (int i = tid; i < TP / 2; i += NW * 32) {
+                const int64_t q = qm + 2 * i;
+                if (q < a.n_m) st_pair(Pm + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
+            }
+        }
+    }
+    for (int x = 0; x < T.n_items; ++x) {
+        const BlockItem& it = T.it[x];
+        const int mt = (it.ncols + 7) >> 3;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+        for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+            const int s = (int)(g % kStages);
+            mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
+            const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
+            const double* rs = rows + (size_t)s * kE * RP + warp * 16 + fr;
+            const double* cs = coef + (size_t)s * kE * CP + fr;
+            // warp-uniform branch per item: only the item's M tiles are issued
+            // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
+            if (mt > 1)
+                item_stage<2, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
+            else
+                item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
+        }
+        const uint64_t keep = l2_policy_last();  // the steps read P next
+        // flush into P (this CTA owns the tile, items in table order, so the
+        // sum of each step is deterministic): the first item of a step stores,
+        // later ones (and every tail item) add — loads first, one round trip.
+        // A step's row can sit in another lane than in the previous item (only
+        // this warp touches these points): the warp barrier orders the accesses.
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int r = 8 * i + fr;
+            if (i >= mt || r >= it.ncols) continue;
+            double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
+            const bool add = T.accumulate || !((it.first_mask >> r) & 1);
+            double2 old[NT];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int64_t q = qm + warp * 16 + 8 * j + fk * 2;
+                old[j] = (add && q < a.n_m) ? ld_cg2(out + q) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int64_t q = qm + warp * 16 + 8 * j + fk * 2;
+                if (q >= a.n_m) continue;
+                if (add)
+                    st_pair_hint(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]), keep);
+                else
+                    st_pair_hint(out + q, d[i][j][0], d[i][j][1], keep);
+            }
+        }
+    }
+    }  // tiles
+}
+
+template <int TP, int NS>
 size_t item_block_smem() {
     return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * kItemPitch * sizeof(double) +
-           (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
+           (2 * NS) * sizeof(uint64_t) + (TP / 16) * sizeof(double);
 }
 
 // ------------------------------------------------------------------ ψ tables ---
@@ -1738,6 +1901,15 @@ BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& 
 // Item table of block (kb0, bt) over slices [ts, te) (single member; see
 // fg_block_item_kernel).  Returns false when it does not fit the table or the
 // scratch buffers, and the caller uses the dense kernel.
+// Item width of a plan: plan->item_cols if set (8 or 16), else
+// FGB200_ITEM_COLS, else 16 for ensembles and 8 for a single member.
+int item_cols(const fg_plan* p) {
+    if (p->item_cols == 8 || p->item_cols == 16) return p->item_cols;
+    static const char* e = getenv("FGB200_ITEM_COLS");
+    if (e && (atoi(e) == 8 || atoi(e) == 16)) return atoi(e);
+    return p->B > 1 ? 16 : 8;
+}
+
 bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, ItemTable& T, int64_t row0) {
     memset(&T, 0, sizeof T);
     if (te <= ts) return true;  // no old slices: n_items = 0
@@ -1839,15 +2011,18 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
     // one dense class holding every step (full / short memory): the dense kernel
     // streams it once for all steps; items would re-read it per 8 steps
     // (above kMaxDenseTBlock there is no dense kernel: items it is, each re-reading)
-    if (ng == 1 && g[0].s == 1 && g[0].n == bt && bt > kItemCols && p->tblock <= kMaxDenseTBlock) return false;
+    const int icols = item_cols(p), pitch = icols == 8 ? kItemPitch8 : kItemPitch;
+    T.cols = icols;
+    T.pitch = pitch;
+    if (ng == 1 && g[0].s == 1 && g[0].n == bt && bt > icols && p->tblock <= kMaxDenseTBlock) return false;
     int n = 0;
     int64_t crow = row0;
     for (int x = 0; x < ng; ++x) {
-        for (int c0 = 0; c0 < g[x].n; c0 += kItemCols) {
+        for (int c0 = 0; c0 < g[x].n; c0 += icols) {
             if (n == kMaxItems) return false;
             BlockItem& it = T.it[n++];
             it.stride = (int32_t)g[x].s;
-            it.ncols = g[x].n - c0 < kItemCols ? g[x].n - c0 : kItemCols;
+            it.ncols = g[x].n - c0 < icols ? g[x].n - c0 : icols;
             // the item streams only the slices its own steps use (an 8-step item of
             // a dense class spans its steps' windows, not the whole group)
             int64_t lo = INT64_MAX, hi = INT64_MIN;
@@ -1877,7 +2052,7 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
         const int nb = bt - 64 * w;  // steps of the block in this word
         T.zero_mask[w] = ~seen[w] & (nb >= 64 ? ~0ull : nb <= 0 ? 0ull : ((1ull << nb) - 1));
     }
-    if (crow * kItemPitch > coef_capacity(p)) return false;
+    if (crow * pitch > coef_capacity(p)) return false;
     return true;
 }
 
@@ -1885,7 +2060,7 @@ int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
     if (T.n_items == 0) return FG_OK;
     int max_rows = 0;
     for (int x = 0; x < T.n_items; ++x) max_rows = T.it[x].n_slices > max_rows ? T.it[x].n_slices : max_rows;
-    const int cx = (max_rows * kItemPitch + 255) / 256;
+    const int cx = (max_rows * T.pitch + 255) / 256;
     const int64_t B = a.total_tiles / a.tpm;
     ++g_launches;
     fg_item_coef_kernel<<<dim3((unsigned)(cx < 16 ? cx : 16), (unsigned)T.n_items, (unsigned)(B < 64 ? B : 64)),
@@ -1895,34 +2070,93 @@ int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
 
 // Item partial sums (coefficient rows already built) into Q, then the ordered
 // reduction into P (or directly into P for a single all-steps item).
-int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st,
-                     bool tail = false) {
+constexpr int kItemMainStages = 8;  // two main CTAs per SM: 2 x 70 KB of ring at TP 112
+constexpr int kItemTailStages = 3;  // tail launches run beside the main CTAs
+
+// Item-kernel tile width: two CTAs per SM (two independent rings, so one
+// CTA's flushes overlap the other's stream), so pick the TP (16-point warps)
+// that minimises the busiest CTA's points, ceil(tiles / (2 SMs)) * TP (c2: 586
+// tiles of 112 = 2 per CTA; ensembles of 512-point members: 128, no partial tiles).
+int choose_item_tp(const fg_plan* p) {
+    static const char* force = getenv("FGB200_ITEM_TP");
+    if (force) return atoi(force);
+    const int cands[3] = {112, 128, 96};
+    int best = 128;
+    int64_t best_cost = INT64_MAX;
+    for (int tp : cands) {
+        const int64_t tiles = ((p->n_m + tp - 1) / tp) * p->B;
+        const int64_t cost = ((tiles + 2 * sm_count() - 1) / (2 * sm_count())) * tp;
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = tp;
+        }
+    }
+    return best;
+}
+
+// Item partial sums (coefficient rows already built) straight into P.
+// 8-column tables: fg_block_item8_kernel on the dense kernel's tiling (`a` as
+// built by block_args, TP = tp8), two CTAs per SM.
+int launch_item8_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st, bool tail) {
     void (*kern)(const BlockArgs, const ItemTable) = nullptr;
     size_t smem = 0;
     const bool ens = p->B > 1;
-#define FG_ITEM_PICK(TPV)                                                                                          \
-    kern = tail ? (ens ? fg_block_item_kernel<TPV, kTailStages, true> : fg_block_item_kernel<TPV, kTailStages, false>) \
-                : (ens ? fg_block_item_kernel<TPV, kMainStages, true> : fg_block_item_kernel<TPV, kMainStages, false>); \
-    smem = tail ? item_block_smem<TPV, kTailStages>() : item_block_smem<TPV, kMainStages>();
+#define FG_ITEM8_PICK(TPV)                                                                                    \
+    kern = tail ? (ens ? fg_block_item8_kernel<TPV, kTailStages, true> : fg_block_item8_kernel<TPV, kTailStages, false>) \
+                : (ens ? fg_block_item8_kernel<TPV, kMainStages, true> : fg_block_item8_kernel<TPV, kMainStages, false>); \
+    smem = tail ? item8_block_smem<TPV, kTailStages>() : item8_block_smem<TPV, kMainStages>();
     switch (tp) {
-        case 128: FG_ITEM_PICK(128) break;
-        case 192: FG_ITEM_PICK(192) break;
-        case 224: FG_ITEM_PICK(224) break;
-        default: FG_ITEM_PICK(256) tp = 256; break;
+        case 128: FG_ITEM8_PICK(128) break;
+        case 192: FG_ITEM8_PICK(192) break;
+        case 224: FG_ITEM8_PICK(224) break;
+        default: FG_ITEM8_PICK(256) tp = 256; break;
     }
-#undef FG_ITEM_PICK
+#undef FG_ITEM8_PICK
     if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                             "item smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
-    // one CTA per tile (at most FGB200_BLOCK_CTAS_PER_SM per SM, looping over
-    // tiles — ensembles too) walks all items: it owns the tile's P rows, so the
-    // items' adds need no atomics
     const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
     const int per = e ? atoi(e) : 2;
     const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
     ++g_launches;
     kern<<<(unsigned)(a.total_tiles < cap ? a.total_tiles : cap), tp + 32, smem, st>>>(a, T);
+    return cuda_check(cudaGetLastError(), "fg_block_item8 launch");
+}
+
+int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st,
+                     bool tail = false) {
+    void (*kern)(const BlockArgs, const ItemTable) = nullptr;
+    size_t smem = 0;
+    int threads = 0;
+    const bool ens = p->B > 1;
+#define FG_ITEM_PICK(TPV)                                                                                  \
+    kern = tail ? (ens ? fg_block_item_kernel<TPV, kItemTailStages, true>                                  \
+                       : fg_block_item_kernel<TPV, kItemTailStages, false>)                                \
+                : (ens ? fg_block_item_kernel<TPV, kItemMainStages, true>                                  \
+                       : fg_block_item_kernel<TPV, kItemMainStages, false>);                               \
+    smem = tail ? item_block_smem<TPV, kItemTailStages>() : item_block_smem<TPV, kItemMainStages>();       \
+    threads = item_threads<TPV>();
+    switch (tp) {
+        case 96: FG_ITEM_PICK(96) break;
+        case 112: FG_ITEM_PICK(112) break;
+        case 128: FG_ITEM_PICK(128) break;
+        default: return fail(FG_ERR_ARG, "item kernel: unsupported tile width %d", tp);
+    }
+#undef FG_ITEM_PICK
+    if (tp * a.tpm < a.n_m || a.tpm * (a.total_tiles / a.tpm) != a.total_tiles)
+        return fail(FG_ERR_ARG, "item kernel: tiles do not match the tile width");
+    if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                            "item smem attribute"))
+        return rc;
+    if (int rc = prefer_max_smem((const void*)kern)) return rc;
+    // two CTAs per SM (FGB200_BLOCK_CTAS_PER_SM) loop over tiles and walk all
+    // items per tile: a CTA owns its tile's P rows, so the items' adds need no atomics
+    const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
+    const int per = e ? atoi(e) : 2;
+    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
+    ++g_launches;
+    kern<<<(unsigned)(a.total_tiles < cap ? a.total_tiles : cap), threads, smem, st>>>(a, T);
     return cuda_check(cudaGetLastError(), "fg_block_item launch");
 }
 
@@ -1969,6 +2203,15 @@ int64_t tail_begin(const fg_plan* p, int64_t kb0) { return kb0 - p->tblock > 0 ?
 // issues it on a side stream while the previous block's steps run.  Single
 // member: coefficient buffer = [tail rows][main rows]; the tail's rows are
 // built here too so the tail launch (on the critical path) only multiplies.
+// The item kernel's own tiling of the same block arguments.
+BlockArgs item_args(const fg_plan* p, const BlockArgs& a, int* tp) {
+    BlockArgs r = a;
+    *tp = choose_item_tp(p);
+    r.tpm = (int32_t)((p->n_m + *tp - 1) / *tp);
+    r.total_tiles = (int32_t)(r.tpm * p->B);
+    return r;
+}
+
 int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     if (kb0 <= 0) {  // nothing older than the block: P = 0
         return cuda_check(cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
@@ -1997,7 +2240,8 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         } else {
             if (int rc = launch_dense_coef(p, tail, st)) return rc;
             const int64_t cp = p->tblock + 4;
-            row0 = (p->tblock * cp + kItemPitch - 1) / kItemPitch;  // dense tail rows, in item-pitch rows
+            const int ip = item_cols(p) == 8 ? kItemPitch8 : kItemPitch;
+            row0 = (p->tblock * cp + ip - 1) / ip;  // dense tail rows, in item-pitch rows
         }
         ItemTable T;
         const bool ok = items_enabled() || p->tblock > kMaxDenseTBlock;
@@ -2006,14 +2250,20 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
                 return cuda_check(
                     cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
                     "P reset");
-            if (int rc = launch_item_coef(a, T, st)) return rc;
-            return launch_item_sums(p, a, T, v.tp, st);
+            if (T.cols == 8) {
+                if (int rc = launch_item_coef(a, T, st)) return rc;
+                return launch_item8_sums(p, a, T, v.tp, st, false);
+            }
+            int itp = 0;
+            const BlockArgs ai = item_args(p, a, &itp);
+            if (int rc = launch_item_coef(ai, T, st)) return rc;
+            return launch_item_sums(p, ai, T, itp, st);
         }
         if (p->tblock > kMaxDenseTBlock)
             return fail(FG_ERR_UNSUPPORTED, "tblock %d: block %lld does not fit the item table", (int)p->tblock,
                         (long long)kb0);
         if (!ens) {
-            a.gcoef += row0 * kItemPitch;
+            a.gcoef += row0 * (item_cols(p) == 8 ? kItemPitch8 : kItemPitch);
             if (int rc = launch_dense_coef(p, a, st)) return rc;
         }
     }
@@ -2041,7 +2291,10 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         if (build_items(p, kb0, bt, a.t_begin, a.t_end, T, 0)) {
             if (T.n_items == 0) return FG_OK;
             T.accumulate = 1;
-            return launch_item_sums(p, a, T, v.tp, st, true);
+            if (T.cols == 8) return launch_item8_sums(p, a, T, v.tp, st, true);
+            int itp = 0;
+            const BlockArgs ai = item_args(p, a, &itp);
+            return launch_item_sums(p, ai, T, itp, st, true);
         }
         if (p->B == 1 || p->tblock > kMaxDenseTBlock)
             return fail(FG_ERR_UNSUPPORTED, "tblock %d: tail of block %lld does not fit the item table",
@@ -2708,7 +2961,8 @@ int fg_block_partials(const fg_plan* p, int64_t kb0, int32_t bt, void* stream) {
 }
 
 int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t base, int64_t horizon,
-                       int64_t* max_rows) {
+                       int32_t item_cols, int64_t* max_rows) {
+    if (item_cols != 8 && item_cols != 16) return fail(FG_ERR_ARG, "fg_block_item_rows: item_cols must be 8 or 16");
     if (n_steps < 0 || tblock < 1 || tblock > kMaxTBlock || !max_rows)
         return fail(FG_ERR_ARG, "fg_block_item_rows: bad arguments");
     fg_plan q;
@@ -2718,6 +2972,7 @@ int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t ba
     q.horizon_max = horizon;
     q.tblock = tblock;
     q.coef_rows = INT64_MAX / (4 * kCoefRow);  // no capacity limit while measuring
+    q.item_cols = item_cols;
     int64_t worst = 0;
     static thread_local ItemTable T;
     for (int64_t kb0 = tblock; kb0 < n_steps; kb0 += tblock) {
@@ -2743,7 +2998,9 @@ int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t ba
 }
 
 int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64_t te, int64_t base,
-                        int64_t horizon, int32_t tblock, int64_t* out, int32_t cap, int32_t* n_items) {
+                        int64_t horizon, int32_t tblock, int32_t item_cols, int64_t* out, int32_t cap,
+                        int32_t* n_items) {
+    if (item_cols != 8 && item_cols != 16) return fail(FG_ERR_ARG, "fg_block_item_table: item_cols must be 8 or 16");
     if (kb0 < 0 || bt < 1 || bt > kMaxTBlock || tblock < bt || tblock > kMaxTBlock || ts < 0 || te > kb0 || !out ||
         !n_items)
         return fail(FG_ERR_ARG, "fg_block_item_table: bad arguments");
@@ -2754,6 +3011,7 @@ int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64
     q.horizon_max = horizon;
     q.tblock = tblock;
     q.coef_rows = INT64_MAX / (4 * kCoefRow);
+    q.item_cols = item_cols;
     static thread_local ItemTable T;
     if (!build_items(&q, kb0, bt, ts, te, T, 0)) {
         *n_items = -1;  // not itemized (dense class or table overflow)
@@ -2762,7 +3020,7 @@ int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64
     *n_items = T.n_items;
     if (T.n_items > cap) return fail(FG_ERR_ARG, "fg_block_item_table: %d items > cap %d", T.n_items, cap);
     for (int x = 0; x < T.n_items; ++x) {
-        int64_t* o = out + (int64_t)x * 12;
+        int64_t* o = out + (int64_t)x * (4 + kItemCols);
         o[0] = T.it[x].t_first;
         o[1] = T.it[x].stride;
         o[2] = T.it[x].n_slices;

@@ -422,6 +422,16 @@ def test_wide_temporal_blocking_matches_goldens(fg, golden, name, tblock):
     test_temporal_blocking_matches_goldens(fg, golden, name, tblock)
 
 
+@pytest.mark.parametrize("cols", ["8", "16"])
+@pytest.mark.parametrize("name", ["c2_small", "point_adaptive3", "batch_adaptive", "3d_sat_adaptive"])
+def test_item_widths_match_goldens(fg, golden, name, cols, monkeypatch):
+    """Both item widths (8-column items on wide tiles, 16-column items on
+    narrow tiles) for single fields and ensembles, at tblock 32 and 128."""
+    monkeypatch.setenv("FGB200_ITEM_COLS", cols)
+    for tb in (32, 128):
+        test_temporal_blocking_matches_goldens(fg, golden, name, tb)
+
+
 def test_wide_temporal_blocking_rejects_dense_plans(fg, golden):
     cfg = _any_field_config(fg, golden, "point_full")
     with pytest.raises(ValueError, match="tblock 64"):

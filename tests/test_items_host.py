@@ -18,12 +18,12 @@ from paper_1004_5128_b200 import _lib
 CAP = 200
 
 
-def item_table(kind, kb0, bt, ts, te, base, tblock):
+def item_table(kind, kb0, bt, ts, te, base, tblock, cols=8):
     L = _lib.load()
-    out = (C.c_int64 * (12 * CAP))()
+    out = (C.c_int64 * (20 * CAP))()
     n = C.c_int32(0)
-    _lib.check(L.fg_block_item_table(kind, kb0, bt, ts, te, base, 0, tblock, out, CAP, C.byref(n)))
-    arr = np.frombuffer(out, dtype=np.int64).reshape(CAP, 12)
+    _lib.check(L.fg_block_item_table(kind, kb0, bt, ts, te, base, 0, tblock, cols, out, CAP, C.byref(n)))
+    arr = np.frombuffer(out, dtype=np.int64).reshape(CAP, 20)
     return n.value, arr[: max(n.value, 0)]
 
 
@@ -37,18 +37,18 @@ def weight(segs, m):
     return 0
 
 
-def check_ownership(kb0, bt, ts, te, base, tblock):
+def check_ownership(kb0, bt, ts, te, base, tblock, cols=8):
     from oracle import fg_oracle as fo
 
-    n, items = item_table(2, kb0, bt, ts, te, base, tblock)
+    n, items = item_table(2, kb0, bt, ts, te, base, tblock, cols)
     if n < 0:
         return None
     segs = [fo.schedule_segments("adaptive", kb0 + b, base) for b in range(bt)]
     owned = {}
-    for t_first, stride, n_sl, ncols, *cols in items.tolist():
-        assert 1 <= ncols <= 8 and stride >= 1 and n_sl >= 1
+    for t_first, stride, n_sl, ncols, *steps in items.tolist():
+        assert 1 <= ncols <= cols and stride >= 1 and n_sl >= 1
         assert ts <= t_first and t_first + (n_sl - 1) * stride < te
-        for b in cols[:ncols]:
+        for b in steps[:ncols]:
             for j in range(n_sl):
                 t = t_first + j * stride
                 if weight(segs[b], kb0 + b - t) == stride:
@@ -64,9 +64,10 @@ def check_ownership(kb0, bt, ts, te, base, tblock):
     return n
 
 
+@pytest.mark.parametrize("cols", [8, 16])
 @pytest.mark.parametrize("base", [2, 3, 5, 8])
 @pytest.mark.parametrize("tblock", [8, 16, 24, 32, 48, 64, 80, 128])
-def test_every_entry_owned_once(base, tblock):
+def test_every_entry_owned_once(base, tblock, cols):
     """Tails ([kb0 - tblock, kb0)) and main ranges ([0, kb0 - tblock)) of the
     first blocks (where the adaptive tail rule and the dense window share a
     class near t = 0) and of later blocks."""
@@ -74,7 +75,7 @@ def test_every_entry_owned_once(base, tblock):
     for kb0 in list(range(tblock, 12 * tblock + 1, tblock)) + [1000 // tblock * tblock, 2496 // tblock * tblock]:
         tb0 = max(0, kb0 - tblock)
         for ts, te in ((tb0, kb0), (0, tb0)):
-            if te > ts and check_ownership(kb0, tblock, ts, te, base, tblock) is not None:
+            if te > ts and check_ownership(kb0, tblock, ts, te, base, tblock, cols) is not None:
                 n_itemized += 1
     assert n_itemized > 0
 
@@ -86,17 +87,18 @@ def test_overlapping_groups_regression():
     assert check_ownership(16, 16, 0, 16, 5, 16) is not None
 
 
-def test_item_rows_bound_covers_blocks():
+@pytest.mark.parametrize("cols", [8, 16])
+def test_item_rows_bound_covers_blocks(cols):
     L = _lib.load()
     rows = C.c_int64(0)
-    _lib.check(L.fg_block_item_rows(2, 1200, 48, 5, 0, C.byref(rows)))
+    _lib.check(L.fg_block_item_rows(2, 1200, 48, 5, 0, cols, C.byref(rows)))
     worst = 0
     for kb0 in range(48, 1200, 48):
         bt = min(48, 1200 - kb0)
         tot = 0
         for ts, te in ((kb0 - 48, kb0), (0, kb0 - 48)):
             if te > ts:
-                n, items = item_table(2, kb0, bt, ts, te, 5, 48)
+                n, items = item_table(2, kb0, bt, ts, te, 5, 48, cols)
                 tot += int(items[:, 2].sum()) if n > 0 else 0
         worst = max(worst, tot)
     assert rows.value == worst > 0
