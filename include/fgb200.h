@@ -97,7 +97,11 @@ typedef struct fg_plan {
     const double* psi_host;      /* optional, single member: host copy of psi_dev[0..tblock]
                                     (blocked steps then get their coefficients as
                                     launch parameters); NULL = read psi_dev       */
-    int64_t q_rows;              /* reserved, 0                                      */
+    int64_t subblock;            /* sub-block launches: S > 0 divides tblock (adaptive,
+                                    blkcoef_dev); each finished S-step sub-block's
+                                    slices are added into the P rows of the block's
+                                    steps two sub-blocks on, so steps sum only
+                                    offsets < 2S themselves; 0 = off              */
     int64_t coef_rows;           /* rows per blkcoef buffer (0 = h_slices)          */
 } fg_plan;
 

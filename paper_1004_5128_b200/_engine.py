@@ -113,6 +113,27 @@ def large_field(p: "Problem") -> bool:
     return p.batch * p.n_m >= 1 << 19
 
 
+def default_subblock(p: "Problem", tblock: int) -> int:
+    """Sub-block length S of the sub-block launches (fg_plan.subblock, 0 = off).
+
+    Large fields (c3, c4, c5) at tblock 128: the block's own slices do not fit
+    in L2, so every step re-reads its recent slices from HBM; with sub-blocks
+    each finished one is streamed once into the later steps' partial sums.
+    Measured on B200 (ms per run, S = 0 / 8 / 16 / 32): c5 1403 / 1492 / 1372 /
+    1350, c3-adaptive 335 / 423 / 339 / 323 — the steps' recent sums are bound
+    by their rounds of loads in flight more than by their count, so only the
+    longest sub-blocks pay.  FGB200_SUBBLOCK overrides (0 disables).
+    """
+    env = os.environ.get("FGB200_SUBBLOCK")
+    if env is not None:
+        s = int(env)
+    else:
+        s = 32 if large_field(p) and tblock >= 128 else 0
+    if s and (tblock % s or tblock // s > 16 or s < 2):
+        return 0
+    return s
+
+
 def round_up(n: int, m: int) -> int:
     return (n + m - 1) // m * m
 
@@ -426,6 +447,8 @@ class Stepper:
                 self.psi_host = np.ascontiguousarray(self.psi[0, : tb + 1].cpu().numpy())
                 plan.psi_host = self.psi_host.ctypes.data
 
+        if plan.tblock and p.kind == "adaptive" and plan.blkcoef_dev:
+            plan.subblock = default_subblock(p, int(plan.tblock))
         self.tblock = int(plan.tblock)
         self.plan = plan
         self.k = 0

@@ -77,7 +77,7 @@ class FgPlan(C.Structure):
         ("P_dev", C.c_void_p),
         ("blkcoef_dev", C.c_void_p),
         ("psi_host", C.c_void_p),
-        ("q_rows", C.c_int64),
+        ("subblock", C.c_int64),
         ("coef_rows", C.c_int64),
     ]
 

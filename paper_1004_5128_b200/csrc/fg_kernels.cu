@@ -65,6 +65,7 @@ constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
 constexpr int kMaxTBlock = 128;  // largest temporal-blocking factor (> 32: itemized stages only)
+constexpr int kMaxSub = 16;      // most sub-blocks per temporal block (plan->subblock)
 constexpr int kMaxDenseTBlock = 32;  // largest factor of the dense block kernel
 constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxDenseTBlock + 4)
 
@@ -1623,6 +1624,11 @@ int validate_plan(const fg_plan* p) {
     if (p->B > 1 && p->blkcoef_dev && p->kind != FG_MEM_ADAPTIVE)
         return fail(FG_ERR_UNSUPPORTED, "ensemble coefficient rows (blkcoef_dev) are for adaptive plans only");
     if (p->tblock && !p->P_dev) return fail(FG_ERR_ARG, "temporal blocking needs P_dev");
+    if (p->subblock < 0 || (p->subblock > 0 && (!p->tblock || p->subblock < 2 || p->tblock % p->subblock != 0 ||
+                                                p->tblock / p->subblock > kMaxSub || !p->blkcoef_dev ||
+                                                p->kind != FG_MEM_ADAPTIVE)))
+        return fail(FG_ERR_ARG, "subblock must be 0, or divide tblock into at most %d parts (adaptive, blkcoef_dev)",
+                    kMaxSub);
     if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
         FgSeg s[FG_MAX_SEGS];
         const int n = fg_segments(p->kind, p->h_slices, p->base, p->horizon_max > 0 ? p->horizon_max : 0, s);
@@ -1746,8 +1752,10 @@ double* block_coef(const fg_plan* p, int64_t kb0) {
 
 // Recent-weight rows of a temporal block: a.rw[k-kb0][m] = weight of offset m in
 // the schedule of step k (1 <= m <= k-kb0), for k in [k0, k1).
-void fill_recent(StepArgs& a, const fg_plan* p, int64_t kb0, int64_t k) {
-    a.rn = recent_list(p->kind, k, kb0, p->base, a.hz_max, a.rm, a.rwt, &a.rw1);
+// t_min: oldest slice the step still sums itself (kb0, or later when sub-block
+// launches have added the older slices of the block into P).
+void fill_recent(StepArgs& a, const fg_plan* p, int64_t t_min, int64_t k) {
+    a.rn = recent_list(p->kind, k, t_min, p->base, a.hz_max, a.rm, a.rwt, &a.rw1);
     if (p->psi_host && p->B == 1) {  // host doubles round like __dmul_rn (IEEE, no contraction)
         a.has_rc = 1;
         for (int e = 0; e < a.rn; ++e) a.rc[e] = (double)a.rwt[e] * p->psi_host[a.rm[e]];
@@ -1779,7 +1787,7 @@ size_t acc_smem(int s, int passes) { return (size_t)passes * (size_t)((kThreads 
 // One step, one launch; grid = one CTA per tile.  kb0 >= 0: temporal-blocking
 // mode, slices t < kb0 are taken from plan->P_dev (block starting at kb0).
 int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, int pdl_wait, int pdl_trigger,
-                  int64_t kb0 = -1) {
+                  int64_t kb0 = -1, int64_t t_min = -1) {
     const int s = choose_split(p);
     StepArgs a = make_args(p, s);
     a.k0 = k;
@@ -1792,7 +1800,7 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
         a.blocked = 1;
         a.kb0 = kb0;
         a.P = block_P(p, kb0);
-        fill_recent(a, p, kb0, k);
+        fill_recent(a, p, t_min >= 0 ? t_min : kb0, k);
     }
     StepKernel kern = pick_kernel(p->ndim, p->reaction, s, kb0 >= 0);
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
@@ -1910,7 +1918,8 @@ int item_cols(const fg_plan* p) {
     return p->B > 1 ? 16 : 8;
 }
 
-bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, ItemTable& T, int64_t row0) {
+bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, ItemTable& T, int64_t row0,
+                 int b_lo = 0) {
     memset(&T, 0, sizeof T);
     if (te <= ts) return true;  // no old slices: n_items = 0
     const int64_t hz = p->kind == 1 ? p->horizon_max : 0;
@@ -1925,7 +1934,7 @@ bool build_items(const fg_plan* p, int64_t kb0, int bt, int64_t ts, int64_t te, 
     static thread_local Grp g[kMaxItems];
     int ng = 0;
     FgSeg segs[FG_MAX_SEGS];
-    for (int b = 0; b < bt; ++b) {
+    for (int b = b_lo; b < bt; ++b) {  // b_lo: sub-block launches feed only the later steps
         const int64_t k = kb0 + b;
         const int ns = fg_segments(p->kind, k, p->base, hz, segs);
         if (ns < 0 || ns > kBlkSegs) return false;  // the coefficient kernel keeps kBlkSegs
@@ -2307,6 +2316,61 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     ++g_launches;
     v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
+}
+
+// Sub-block launch (plan->subblock = S > 0): the slices of sub-block i of the
+// block kb0, [kb0 + iS, kb0 + (i+1)S), added into the P rows of the block's
+// steps b >= (i+2)S.  Those steps then sum themselves only the slices of their
+// own and the previous sub-block (recent offsets < 2S instead of < tblock), so
+// a slice of a large field is streamed once by this launch instead of once by
+// every later step of the block.  Runs on the library's sub-block stream while
+// sub-block i+1's steps run; sub-block i+2 joins it.  Coefficient rows reuse
+// the block's buffer from row 0 (its tail and main launches are done).
+int launch_block_partial(const fg_plan* p, int64_t kb0, int bt, int i, cudaStream_t st) {
+    const int64_t S = p->subblock;
+    const int b_lo = (int)((i + 2) * S);
+    if (b_lo >= bt) return FG_OK;
+    const BlockVariant v = choose_block_variant(p, true);
+    if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
+    BlockArgs a = block_args(p, kb0, bt, v);
+    a.t_begin = kb0 + i * S;
+    a.t_end = kb0 + (i + 1) * S;
+    a.accumulate = 1;
+    ItemTable T;
+    if (!a.gcoef || !build_items(p, kb0, bt, a.t_begin, a.t_end, T, 0, b_lo))
+        return fail(FG_ERR_UNSUPPORTED, "sub-block %d of block %lld does not fit the item table", i, (long long)kb0);
+    if (T.n_items == 0) return FG_OK;
+    T.accumulate = 1;
+    if (T.cols == 8) {
+        if (int rc = launch_item_coef(a, T, st)) return rc;
+        return launch_item8_sums(p, a, T, v.tp, st, true);
+    }
+    int itp = 0;
+    const BlockArgs ai = item_args(p, a, &itp);
+    if (int rc = launch_item_coef(ai, T, st)) return rc;
+    return launch_item_sums(p, ai, T, itp, st, true);
+}
+
+// Per-thread sub-block stream and its events (one completion event per
+// sub-block of a block, kMaxSub at most).
+int sub_stream(cudaStream_t* s, cudaEvent_t* ready, cudaEvent_t* done) {
+    static thread_local int dev = -1;
+    static thread_local cudaStream_t ss = nullptr;
+    static thread_local cudaEvent_t er = nullptr, ed[kMaxSub] = {};
+    int cur = 0;
+    if (int rc = cuda_check(cudaGetDevice(&cur), "cudaGetDevice")) return rc;
+    if (!ss || dev != cur) {
+        if (int rc = cuda_check(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking), "sub-block stream")) return rc;
+        if (int rc = cuda_check(cudaEventCreateWithFlags(&er, cudaEventDisableTiming), "sub-block event")) return rc;
+        for (int i = 0; i < kMaxSub; ++i)
+            if (int rc = cuda_check(cudaEventCreateWithFlags(&ed[i], cudaEventDisableTiming), "sub-block event"))
+                return rc;
+        dev = cur;
+    }
+    *s = ss;
+    *ready = er;
+    for (int i = 0; i < kMaxSub; ++i) done[i] = ed[i];
+    return FG_OK;
 }
 
 // Debug timeline of the temporal-blocking pipeline (FGB200_TRACE=<file>, not in
@@ -2742,7 +2806,9 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
     }
     double* ppool = n_snap > 0 ? pool : nullptr;
     // chain launches (one per temporal block, tiles synchronised pairwise)
-    const bool chain = (flags & FG_RUN_CHAIN) && !persistent && tb && chain_fits(p);
+    const bool chain = (flags & FG_RUN_CHAIN) && !persistent && tb && chain_fits(p) && p->subblock == 0;
+    // sub-block launches (per-step launch modes only)
+    const bool sub = tb && p->subblock > 0 && !persistent && !chain;
     if (chain) {
         ChainScratch* cs = nullptr;  // allocated here, never inside a graph capture
         if (int rc = chain_scratch(tiles_of(p, 1), &cs)) return rc;
@@ -2817,7 +2883,13 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
                 ++si;
             }
             const bool wait = pdl && k > k0 && !(k == ka && first_after_block);
-            if (int r = launch_single(p, k, snap, cap, wait, pdl, kb0)) return r;
+            // sub-blocks: slices older than the previous sub-block are in P already
+            int64_t t_min = kb0;
+            if (kb0 >= 0 && p->subblock > 0) {
+                const int64_t i = (k - kb0) / p->subblock;
+                t_min = kb0 + (i > 0 ? (i - 1) * p->subblock : 0);
+            }
+            if (int r = launch_single(p, k, snap, cap, wait, pdl, kb0, t_min)) return r;
             if (snap)
                 if (int r = copy_out(i, i + 1)) return r;
         }
@@ -2841,6 +2913,44 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         if (int r = launch_chain(p, ka, kz, kb0, pool, sst, ssl, ns, cap)) return r;
         si = j;
         return copy_out(i0, si);
+    };
+    // the steps [ks, ke) of block kb with sub-block launches (plan->subblock)
+    cudaStream_t sstream = nullptr;
+    cudaEvent_t sready = nullptr, sdone[kMaxSub] = {};
+    auto sub_steps = [&](int64_t ks, int64_t ke, int64_t kb, int bt, bool start) -> int {
+        const int64_t S = p->subblock;
+        bool pending[kMaxSub] = {};
+        bool after_join = start;
+        if (start && ks > kb) {  // P recomputed mid-block: add the finished sub-blocks first
+            for (int i = 0; kb + (i + 1) * S <= ks; ++i)
+                if (int r = launch_block_partial(p, kb, bt, i, cap)) return r;
+        }
+        int r = FG_OK;
+        for (int64_t k = ks; k < ke && r == FG_OK;) {
+            const int i = (int)((k - kb) / S);
+            const int64_t se = kb + (i + 1) * S < ke ? kb + (i + 1) * S : ke;
+            if (i >= 2 && pending[i - 2]) {
+                r = cuda_check(cudaStreamWaitEvent(cap, sdone[i - 2], 0), "sub-block join");
+                pending[i - 2] = false;
+                after_join = true;
+            }
+            if (r == FG_OK) r = steps(k, se, kb, after_join);
+            after_join = false;
+            if (r == FG_OK && se == kb + (i + 1) * S && (i + 2) * S < bt) {  // sub-block i is complete
+                r = cuda_check(cudaEventRecord(sready, cap), "sub-block fork");
+                if (r == FG_OK) r = cuda_check(cudaStreamWaitEvent(sstream, sready, 0), "sub-block fork wait");
+                if (r == FG_OK) r = launch_block_partial(p, kb, bt, i, sstream);
+                if (r == FG_OK) r = cuda_check(cudaEventRecord(sdone[i], sstream), "sub-block done");
+                pending[i] = r == FG_OK;
+            }
+            k = se;
+        }
+        for (int i = 0; i < kMaxSub; ++i)  // never leave the sub-block stream unjoined
+            if (pending[i]) {
+                const int r2 = cuda_check(cudaStreamWaitEvent(cap, sdone[i], 0), "sub-block join");
+                if (r == FG_OK) r = r2;
+            }
+        return r;
     };
     auto persistent_steps = [&](int64_t ka, int64_t kz, int64_t kb0) {
         if (int r = kb0 >= 0 ? launch_persistent(p, ka, kz, ppool, cap, G, passes, s, kb0)
@@ -2870,6 +2980,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         cudaStream_t side = nullptr;
         cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
         if (overlap_enabled()) rc = side_stream(&side, &ev_fork, ev_join);
+        if (rc == FG_OK && sub) rc = sub_stream(&sstream, &sready, sdone);
         int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
         BlockTrace tr(graph ? nullptr : getenv("FGB200_TRACE"));
         for (int64_t kb = k0 - k0 % tb; kb < k1 && rc == FG_OK; kb += tb) {
@@ -2902,6 +3013,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
             }
             rc = persistent ? persistent_steps(ks, ke, kb)
                  : chain    ? chain_steps(ks, ke, kb, start)
+                 : sub      ? sub_steps(ks, ke, kb, block_len(kb), start)
                             : steps(ks, ke, kb, start);
         }
         if (main_on_side >= 0) {  // error path: never leave the side stream unjoined
