@@ -336,8 +336,10 @@ def run_ours(args) -> None:
     if blk:
         blk["share_of_run"] = blk["total_ms"] / (run_s * 1e3)
         achieved = blk["alg_bytes_per_launch"] / (blk["avg_launch_us"] * 1e-6) / 1e9
-        kernel = ("block stage (per block: fg_item_coef_kernel x2 + fg_block_item_kernel main + tail)"
-                  if prob.batch == 1 and prob.kind == "adaptive" else
+        item = "fg_block_item8_kernel" if int(st.plan.item_cols) == 8 else "fg_block_item_kernel"
+        sub = f" + sub-block launches (S={int(st.plan.subblock)})" if int(st.plan.subblock) else ""
+        kernel = (f"block stage (per block: fg_item_coef_kernel + {item} main + tail{sub})"
+                  if prob.kind == "adaptive" else
                   "block stage (per block: coefficient kernels + fg_block_tma_kernel main + tail)")
         traffic = tr["dram_bytes_per_launch"][0] * blk["alg_bytes_per_launch"] / tr["algorithmic_bytes_per_launch"][0] \
             if tr and tr.get("algorithmic_bytes_per_launch") else None

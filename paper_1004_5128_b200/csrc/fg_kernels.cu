@@ -890,6 +890,15 @@ size_t tma_block_smem() {
            (STAGED ? 0 : (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int));
 }
 
+// Item flushes add into P with reductions performed at L2 (no load round trip
+// in the consumer warps).  Still deterministic: a step's row is touched by one
+// lane per item, and the __syncwarp before every flush orders the previous
+// item's store/adds (other lanes) before this one's, so the adds reach each
+// element in table order — the same rounding as the load-add-store they replace.
+__device__ __forceinline__ void red_add(double* p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
@@ -1335,20 +1344,16 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
             if (i >= mt || r >= it.ncols) continue;
             double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
             const bool add = T.accumulate || !((it.first_mask >> r) & 1);
-            double2 old[NT];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const int64_t q = qm + warp * 32 + 8 * j + fk * 2;
-                old[j] = (add && q < a.n_m) ? ld_cg2(out + q) : make_double2(0.0, 0.0);
-            }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 const int64_t q = qm + warp * 32 + 8 * j + fk * 2;
                 if (q >= a.n_m) continue;
-                if (add)
-                    st_pair_hint(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]), keep);
-                else
+                if (add) {  // fire-and-forget L2 adds, applied in program order (see red_add)
+                    red_add(out + q, d[i][j][0]);
+                    red_add(out + q + 1, d[i][j][1]);
+                } else {
                     st_pair_hint(out + q, d[i][j][0], d[i][j][1], keep);
+                }
             }
         }
     }
@@ -1489,20 +1494,16 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
             if (i >= mt || r >= it.ncols) continue;
             double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
             const bool add = T.accumulate || !((it.first_mask >> r) & 1);
-            double2 old[NT];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const int64_t q = qm + warp * 16 + 8 * j + fk * 2;
-                old[j] = (add && q < a.n_m) ? ld_cg2(out + q) : make_double2(0.0, 0.0);
-            }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 const int64_t q = qm + warp * 16 + 8 * j + fk * 2;
                 if (q >= a.n_m) continue;
-                if (add)
-                    st_pair_hint(out + q, __dadd_rn(old[j].x, d[i][j][0]), __dadd_rn(old[j].y, d[i][j][1]), keep);
-                else
+                if (add) {  // fire-and-forget L2 adds, applied in program order (see red_add)
+                    red_add(out + q, d[i][j][0]);
+                    red_add(out + q + 1, d[i][j][1]);
+                } else {
                     st_pair_hint(out + q, d[i][j][0], d[i][j][1], keep);
+                }
             }
         }
     }

@@ -1,8 +1,9 @@
-# A/B: current tree vs build/ab_head (HEAD of the branch): c2 bench alternated + host enqueue rate
+# A/B: current tree vs build/ab_head (HEAD of the branch)
 mkdir -p gpurun_out
 for i in 1 2; do
-  timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ab_new_$i.log 2>&1
-  (cd build/ab_head && timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > ../../gpurun_out/ab_head_$i.log 2>&1)
+  for c in c2 c5 c3-adaptive; do
+  timeout 300 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ab_new_${c}_$i.log 2>&1
+  (cd build/ab_head && timeout 300 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline > ../../gpurun_out/ab_head_${c}_$i.log 2>&1)
+  done
 done
-python scripts/host_rate.py > gpurun_out/ab_host_new.log 2>&1
-(cd build/ab_head && python scripts/host_rate.py > ../../gpurun_out/ab_host_head.log 2>&1)
+timeout 900 python -m pytest tests/test_gpu_block.py tests/test_gpu_parity.py -q -x > gpurun_out/ab_tests.log 2>&1; echo tests=$?
