@@ -107,6 +107,10 @@ __device__ __forceinline__ void st_pair_hint(double* p, double a, double b, uint
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol) : "memory");
 }
 
+__device__ __forceinline__ void st_hint1(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ double2 ld_cg2_hint(const double* p, uint64_t pol) {
     double2 v;
     asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
@@ -601,14 +605,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                     const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
                     constexpr int kR = REACT ? 4 : 5;  // recent slices in flight per round (no spills)
 #pragma unroll 1
+                    // entries oldest first (descending m): the fused pair kernel must
+                    // add the newest ones after its dependency wait, in the same order
                     for (int e0 = 0; e0 < rn; e0 += kR) {
                         double2 v[kR];
                         double c[kR];
 #pragma unroll
                         for (int u = 0; u < kR; ++u) {
-                            const int e = e0 + u;
-                            const int m = e < rn ? rm[e] : 0;
-                            const bool on = e < rn && m <= mmax;
+                            const int e = rn - 1 - (e0 + u);
+                            const int m = e >= 0 ? rm[e] : 0;
+                            const bool on = e >= 0 && m <= mmax;
                             if (on) {
                                 v[u] = ld_stream(hbase - (int64_t)m * a.slice_stride);
                                 c[u] = rcoef ? rcoef[e] : __dmul_rn((double)rwt[e], __ldg(psi_b + m));
@@ -742,6 +748,251 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
         if (a.chain) chain_arrive(a.flags, a.bar, blockIdx.x, (unsigned long long)(k - a.k0 + 1), 1ull);
         else if (multi) grid_arrive(a.bar);
     }
+}
+
+// ------------------------------------------------------- fused step pairs ---
+// Steps k and k+1 of a temporal block in one launch (1D and 2D fields): a CTA
+// computes step k on its tile plus a halo of R points each side (R = 1 in 1D,
+// one row in 2D) from u^k staged in shared memory, then step k+1 on its tile
+// from those values, so the step chain pays one kernel boundary and one L2
+// round trip per two steps.  The halo points' values are recomputed with the
+// very same arithmetic as by their owning CTA (bit-identical results).
+// Before the dependency wait only slices written two launches back are read:
+// step k's recent entries with m >= 3 and step k+1's with m >= 4 (oldest
+// first, the order the single-step kernel uses); m = 2 (step k) and m = 3, 2
+// (step k+1) and the m = 1 terms are added after it.
+// u buffers: the pair reads u^k from `u_in`, writes u^{k+1} of its tile to the
+// parity buffer u[(k+1) & 1] (the divergence report reads it) and u^{k+2} to
+// `u_out`, which no CTA of the launch reads: pairs alternate between a library
+// scratch buffer and the parity buffer u[k & 1], and run in even numbers so the
+// field is back in its parity buffer after each sequence.  *u3_step records
+// which step's field sits in the scratch buffer (fg_u3_fixup_kernel).
+struct PairArgs {
+    StepArgs s;                // step k: shared fields, recent list, P (block kb0)
+    RecentRow r2;              // step k+1's recent list
+    const double* u_in;        // u^k
+    double* u_mid;             // u^{k+1} (own tile) = u[(k+1) & 1]
+    double* u_out;             // u^{k+2}
+    double* snap1;             // snapshot of u^{k+1} (or NULL)
+    double* snap2;             // snapshot of u^{k+2} (or NULL)
+    int64_t* u3_step;
+    int32_t writes_u3;
+};
+constexpr int kPairTile = 512;                 // points per CTA (as the blocked step kernel)
+constexpr int kPairMaxHalo = 256;              // R <= 256
+constexpr int kPairNP = (kPairTile + 2 * kPairMaxHalo + kThreads - 1) / kThreads;  // extended points per thread
+
+template <int NDIM, int REACT>
+__global__ void __launch_bounds__(kThreads, 2) fg_step2_kernel(const __grid_constant__ PairArgs A) {
+    const StepArgs& a = A.s;
+    extern __shared__ double sm2[];
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int64_t b = tile / a.tpm;
+    const int32_t q0 = (tile % a.tpm) * kPairTile;
+    const int32_t n = a.n_m;
+    const int32_t R = NDIM == 1 ? 1 : a.sh.n1;
+    const int32_t o_lo = q0, o_hi = q0 + kPairTile < n ? q0 + kPairTile : n;
+    const int32_t lo = o_lo - R > 0 ? o_lo - R : 0, hi = o_hi + R < n ? o_hi + R : n;    // extended range E
+    const int32_t ulo = lo - R > 0 ? lo - R : 0, uhi = hi + R < n ? hi + R : n;          // u^k staged
+    double* su = sm2;                                  // [uhi - ulo] u^k
+    double* su1 = sm2 + (kPairTile + 4 * kPairMaxHalo);  // [hi - lo]  u^{k+1}
+    const int64_t k = a.k0, bb = k - a.kb0;
+    const int64_t ss = a.slice_stride;
+    const double* Hm = a.H + b * a.ms;                 // member's slice rows
+    const double* psi_b = a.psi + b * a.psi_stride;
+    const bool hc = a.has_rc != 0;
+    const RecentRow& r2 = A.r2;
+    auto coef1 = [&](int e) { return hc ? a.rc[e] : __dmul_rn((double)a.rwt[e], __ldg(psi_b + a.rm[e])); };
+    auto coef2 = [&](int e) { return hc ? r2.rc[e] : __dmul_rn((double)r2.rwt[e], __ldg(psi_b + r2.rm[e])); };
+
+    // ---- A (before the dependency): P rows and the recent entries two launches old
+    double acc1[kPairNP], acc2[kPairNP], pb1[kPairNP], pb2[kPairNP];
+#pragma unroll
+    for (int j = 0; j < kPairNP; ++j) {
+        const int32_t p = lo + tid + j * kThreads;
+        acc1[j] = acc2[j] = pb1[j] = pb2[j] = 0.0;
+        if (p < hi) pb1[j] = ld_cg(a.P + bb * ss + b * a.ms + p);
+        if (p >= o_lo && p < o_hi) pb2[j] = ld_cg(a.P + (bb + 1) * ss + b * a.ms + p);
+    }
+    // rounds of kPR entries x kPairNP points in flight (oldest first); padding
+    // entries add fma(0, 0, acc), which leaves every nonzero partial unchanged
+    // and is normalised away by the __dadd_rn(0, .) below, as in the step kernel
+    constexpr int kPR = 3;
+    {
+        int n1 = 0;  // step k: entries m >= 3 are the last n1 of the list
+        while (n1 < a.rn && a.rm[a.rn - 1 - n1] >= 3) ++n1;
+        for (int e0 = 0; e0 < n1; e0 += kPR) {
+            double v[kPR][kPairNP], c[kPR];
+#pragma unroll
+            for (int u = 0; u < kPR; ++u) {
+                const int e = a.rn - 1 - (e0 + u);
+                const bool on = e0 + u < n1;
+                c[u] = on ? coef1(e) : 0.0;
+                const double* h = Hm + (k - (on ? a.rm[e] : 0)) * ss;
+#pragma unroll
+                for (int j = 0; j < kPairNP; ++j) {
+                    const int32_t p = lo + tid + j * kThreads;
+                    v[u][j] = (on && p < hi) ? ld_cg(h + p) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPR; ++u)
+#pragma unroll
+                for (int j = 0; j < kPairNP; ++j) acc1[j] = fma(c[u], v[u][j], acc1[j]);
+        }
+        int n2 = 0;  // step k+1: entries m >= 4
+        while (n2 < r2.rn && r2.rm[r2.rn - 1 - n2] >= 4) ++n2;
+        for (int e0 = 0; e0 < n2; e0 += kPR) {
+            double v[kPR][kPairNP / 2], c[kPR];
+#pragma unroll
+            for (int u = 0; u < kPR; ++u) {
+                const int e = r2.rn - 1 - (e0 + u);
+                const bool on = e0 + u < n2;
+                c[u] = on ? coef2(e) : 0.0;
+                const double* h = Hm + (k + 1 - (on ? r2.rm[e] : 0)) * ss;
+#pragma unroll
+                for (int j = 0; j < kPairNP; ++j) {
+                    const int32_t p = lo + tid + j * kThreads;
+                    const bool own = p >= o_lo && p < o_hi;
+                    if (j < kPairNP / 2) v[u][j] = 0.0;
+                    if (own) v[u][j % (kPairNP / 2)] = on ? ld_cg(h + p) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPR; ++u)
+#pragma unroll
+                for (int j = 0; j < kPairNP; ++j) {
+                    const int32_t p = lo + tid + j * kThreads;
+                    if (p >= o_lo && p < o_hi) acc2[j] = fma(c[u], v[u][j % (kPairNP / 2)], acc2[j]);
+                }
+        }
+    }
+
+    // ---- dependency on the previous launch (steps k-2, k-1)
+    if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;");
+    const bool live = *(volatile const int64_t*)a.status > k;
+
+    // ---- C: stage u^k, then the newest history terms
+    const double* ub = A.u_in + b * a.ms;
+    for (int32_t i = tid; i < uhi - ulo; i += kThreads) su[i] = ld_cg(ub + ulo + i);
+    double h1[kPairNP], h2[kPairNP];
+#pragma unroll
+    for (int j = 0; j < kPairNP; ++j) {
+        const int32_t p = lo + tid + j * kThreads;
+        h1[j] = h2[j] = 0.0;
+        if (p < hi) {
+            if (k >= 1) h1[j] = ld_cg(Hm + (k - 1) * ss + p);
+            if (k >= 2) h2[j] = ld_cg(Hm + (k - 2) * ss + p);
+        }
+    }
+    __syncthreads();
+    // entries m = 3 / 2 of a list (ascending, so they are the first ones)
+    int e1_2 = -1, e2_2 = -1, e2_3 = -1;
+    for (int e = 0; e < a.rn && a.rm[e] <= 3; ++e)
+        if (a.rm[e] == 2) e1_2 = e;
+    for (int e = 0; e < r2.rn && r2.rm[e] <= 3; ++e) {
+        if (r2.rm[e] == 2) e2_2 = e;
+        if (r2.rm[e] == 3) e2_3 = e;
+    }
+    const int64_t len_k = k + 1;  // kinds full/adaptive (short memory never pairs)
+    const double decay = a.decay[b], diffuse = a.diffuse[b];
+    double d1[kPairNP], u1[kPairNP];
+    // step k on E
+#pragma unroll
+    for (int j = 0; j < kPairNP; ++j) {
+        const int32_t p = lo + tid + j * kThreads;
+        d1[j] = u1[j] = 0.0;
+        if (p >= hi) continue;
+        double acc = acc1[j];
+        if (e1_2 >= 0) acc = fma(coef1(e1_2), h2[j], acc);
+        acc = __dadd_rn(__dadd_rn(0.0, acc), pb1[j]);
+        if (a.rw1 != 0 && len_k >= 2) acc = fma(hc ? a.rc1 : __dmul_rn((double)a.rw1, __ldg(psi_b + 1)), h1[j], acc);
+        const bool in = interior<NDIM>(a.sh, p);
+        const double c = su[p - ulo];
+        double d = 0.0;
+        if (in) {
+            if (NDIM == 1) {
+                d = __dsub_rn(__dadd_rn(su[p + 1 - ulo], su[p - 1 - ulo]), __dmul_rn(2.0, c));
+            } else {
+                double r = __dadd_rn(su[p + R - ulo], su[p - R - ulo]);
+                r = __dsub_rn(r, __dmul_rn(4.0, c));
+                r = __dadd_rn(r, su[p + 1 - ulo]);
+                d = __dadd_rn(r, su[p - 1 - ulo]);
+            }
+        }
+        acc = fma(hc ? a.rc0 : __ldg(psi_b), d, acc);
+        double nu;
+        if (REACT == 0) {
+            nu = __dadd_rn(__dmul_rn(c, decay), __dmul_rn(diffuse, acc));
+        } else {
+            const double f = __ddiv_rn(__dmul_rn(-a.vmax, c), __dadd_rn(a.km, c));
+            nu = __dadd_rn(__dadd_rn(c, __dmul_rn(a.dt[b], f)), __dmul_rn(diffuse, acc));
+        }
+        if (!in) nu = 0.0;
+        d1[j] = d;
+        u1[j] = nu;
+        su1[p - lo] = nu;
+    }
+    __syncthreads();
+    if (!live) return;
+    const uint64_t keep = l2_policy_last(), drop = l2_policy_first();
+    const int64_t moff = b * a.ms;
+    // step k+1 on the tile
+#pragma unroll
+    for (int j = 0; j < kPairNP; ++j) {
+        const int32_t p = lo + tid + j * kThreads;
+        if (p < o_lo || p >= o_hi) continue;
+        double acc = acc2[j];
+        if (e2_3 >= 0) acc = fma(coef2(e2_3), h2[j], acc);
+        if (e2_2 >= 0) acc = fma(coef2(e2_2), h1[j], acc);
+        acc = __dadd_rn(__dadd_rn(0.0, acc), pb2[j]);
+        if (r2.rw1 != 0) acc = fma(hc ? r2.rc1 : __dmul_rn((double)r2.rw1, __ldg(psi_b + 1)), d1[j], acc);
+        const bool in = interior<NDIM>(a.sh, p);
+        const double c = u1[j];
+        double d = 0.0;
+        if (in) {
+            if (NDIM == 1) {
+                d = __dsub_rn(__dadd_rn(su1[p + 1 - lo], su1[p - 1 - lo]), __dmul_rn(2.0, c));
+            } else {
+                double r = __dadd_rn(su1[p + R - lo], su1[p - R - lo]);
+                r = __dsub_rn(r, __dmul_rn(4.0, c));
+                r = __dadd_rn(r, su1[p + 1 - lo]);
+                d = __dadd_rn(r, su1[p - 1 - lo]);
+            }
+        }
+        acc = fma(hc ? r2.rc0 : __ldg(psi_b), d, acc);
+        double nu;
+        if (REACT == 0) {
+            nu = __dadd_rn(__dmul_rn(c, decay), __dmul_rn(diffuse, acc));
+        } else {
+            const double f = __ddiv_rn(__dmul_rn(-a.vmax, c), __dadd_rn(a.km, c));
+            nu = __dadd_rn(__dadd_rn(c, __dmul_rn(a.dt[b], f)), __dmul_rn(diffuse, acc));
+        }
+        if (!in) nu = 0.0;
+        if (!isfinite(u1[j])) atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
+        if (!isfinite(nu)) atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 2));
+        st_hint1(a.H + k * ss + moff + p, d1[j], keep);
+        st_hint1(a.H + (k + 1) * ss + moff + p, d, keep);
+        st_hint1(A.u_mid + moff + p, u1[j], keep);
+        st_hint1(A.u_out + moff + p, nu, keep);
+        if (A.snap1) st_hint1(A.snap1 + moff + p, u1[j], drop);
+        if (A.snap2) st_hint1(A.snap2 + moff + p, nu, drop);
+    }
+    if (tile == 0 && tid == 0) *A.u3_step = A.writes_u3 ? k + 2 : -1;
+}
+
+// After a run with pair launches: when the run stopped at a step whose field
+// sits in the scratch buffer, copy it to its parity buffer (the divergence
+// report and the caller read u[step & 1]).
+__global__ void fg_u3_fixup_kernel(const int64_t* status, const int64_t* u3_step, const double* u3, double* u0,
+                                   double* u1, int64_t n) {
+    const int64_t s = *u3_step;
+    if (s < 0 || *status != s) return;
+    double* dst = (s & 1) ? u1 : u0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = u3[i];
 }
 
 // Recent lists of the steps kb0 .. kb0+bt-1 of a block for chain launches (one
@@ -1821,6 +2072,112 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
     return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "fg_step launch");
 }
 
+// ---- fused step pairs (fg_step2_kernel) -------------------------------------
+// Eligible plans: blocked 1D/2D fields whose halo (one row) is at most
+// kPairMaxHalo points, one warp column per tile (split 1), adaptive or full
+// memory, m = 0 from the stencil.  FGB200_PAIRS=0 disables.
+bool pairs_enabled(const fg_plan* p) {
+    const char* e = getenv("FGB200_PAIRS");  // read per call (tests toggle it)
+    if (e && e[0] == '0') return false;
+    if (!p->tblock || p->tblock % 2 || p->ndim > 2 || p->kind == FG_MEM_SHORT || p->subblock) return false;
+    if (p->step_flags & FG_STEP_M0_FROM_HISTORY) return false;
+    if (choose_split(p) != 1 || tile_points(1) != kPairTile) return false;
+    // default on for 1D only: measured on B200, c1 8.13 -> 7.86 ms, but c2 (2D,
+    // halo = one 256-point row) 33.4 -> 32.9 ms only — a pair CTA recomputes a
+    // halo as large as its tile and needs ~95 registers, so one pair CTA per SM
+    // fits beside the block stage and consecutive pairs barely overlap
+    if (!(e && e[0] == '1') && p->ndim != 1) return false;
+    return (p->ndim == 1 ? 1 : p->shape[1]) <= kPairMaxHalo;
+}
+
+// Library scratch of pair launches: the alternate field buffer and *u3_step.
+struct PairScratch {
+    int dev = -1;
+    double* u3 = nullptr;
+    int64_t n = 0;
+    int64_t* step = nullptr;
+    ~PairScratch() {
+        if (u3) cudaFree(u3);
+        if (step) cudaFree(step);
+    }
+};
+
+int pair_scratch(const fg_plan* p, PairScratch** out) {
+    static thread_local PairScratch ps;
+    int cur = 0;
+    if (int rc = cuda_check(cudaGetDevice(&cur), "cudaGetDevice")) return rc;
+    const int64_t n = p->B * p->ms;
+    if (ps.dev != cur || ps.n < n) {
+        if (ps.u3) cudaFree(ps.u3);
+        if (ps.step) cudaFree(ps.step);
+        ps.u3 = nullptr;
+        ps.step = nullptr;
+        if (int rc = cuda_check(cudaMalloc(&ps.u3, (size_t)n * sizeof(double)), "pair field buffer")) return rc;
+        if (int rc = cuda_check(cudaMalloc(&ps.step, sizeof(int64_t)), "pair step")) return rc;
+        ps.n = n;
+        ps.dev = cur;
+    }
+    *out = &ps;
+    return FG_OK;
+}
+
+constexpr size_t kPairSmem = (size_t)(kPairTile + 4 * kPairMaxHalo + kPairTile + 2 * kPairMaxHalo) * sizeof(double);
+
+// Steps k, k+1 of block kb0 in one launch.
+int launch_pair(const fg_plan* p, int64_t k, int64_t kb0, double* snap1, double* snap2, cudaStream_t st,
+                int pdl_wait, int pdl_trigger, const double* u_in, double* u_mid, double* u_out, int writes_u3,
+                int64_t* u3_step) {
+    static thread_local PairArgs A;  // ~3 KB: not on the stack of every caller
+    memset(&A, 0, sizeof A);
+    StepArgs& a = A.s;
+    a = make_args(p, 1);
+    a.k0 = k;
+    a.k1 = k + 2;
+    a.passes = 1;
+    a.pdl_wait = pdl_wait;
+    a.pdl_trigger = pdl_trigger;
+    a.blocked = 1;
+    a.kb0 = kb0;
+    a.P = block_P(p, kb0);
+    fill_recent(a, p, kb0, k);
+    StepArgs b2;  // step k+1's list, in a scratch StepArgs
+    memset(&b2, 0, sizeof b2);
+    b2.hz_max = a.hz_max;
+    fill_recent(b2, p, kb0, k + 1);
+    A.r2.rn = b2.rn;
+    A.r2.rw1 = b2.rw1;
+    A.r2.rc0 = b2.rc0;
+    A.r2.rc1 = b2.rc1;
+    memcpy(A.r2.rm, b2.rm, sizeof A.r2.rm);
+    memcpy(A.r2.rwt, b2.rwt, sizeof A.r2.rwt);
+    memcpy(A.r2.rc, b2.rc, sizeof A.r2.rc);
+    A.u_in = u_in;
+    A.u_mid = u_mid;
+    A.u_out = u_out;
+    A.snap1 = snap1;
+    A.snap2 = snap2;
+    A.u3_step = u3_step;
+    A.writes_u3 = writes_u3;
+    void (*kern)(const PairArgs) = nullptr;
+    if (p->ndim == 1) kern = p->reaction ? fg_step2_kernel<1, 1> : fg_step2_kernel<1, 0>;
+    else kern = p->reaction ? fg_step2_kernel<2, 1> : fg_step2_kernel<2, 0>;
+    if (int rc = prefer_max_smem((const void*)kern)) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.total_tiles, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kPairSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (pdl_wait) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    ++g_launches;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, A), "fg_step2 launch");
+}
+
 typedef void (*BlockKernel)(const BlockArgs);
 
 struct BlockVariant {
@@ -2810,6 +3167,12 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
     const bool chain = (flags & FG_RUN_CHAIN) && !persistent && tb && chain_fits(p) && p->subblock == 0;
     // sub-block launches (per-step launch modes only)
     const bool sub = tb && p->subblock > 0 && !persistent && !chain;
+    // fused step pairs (per-step launch modes, small 1D/2D fields)
+    const bool pairs = tb && !persistent && !chain && !sub && pairs_enabled(p);
+    PairScratch* ps = nullptr;
+    if (pairs) {  // allocated here, never inside a graph capture
+        if (int rc = pair_scratch(p, &ps)) return rc;
+    }
     if (chain) {
         ChainScratch* cs = nullptr;  // allocated here, never inside a graph capture
         if (int rc = chain_scratch(tiles_of(p, 1), &cs)) return rc;
@@ -2915,6 +3278,32 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         si = j;
         return copy_out(i0, si);
     };
+    // the steps [ka, kz) of block kb0 as fused pairs (an even number of them, so
+    // the field is back in its parity buffer), then single steps for the rest
+    auto pair_steps = [&](int64_t ka, int64_t kz, int64_t kb0, bool first) -> int {
+        int64_t npairs = (kz - ka) / 2;
+        if (npairs % 2) --npairs;
+        int64_t k = ka;
+        for (int64_t i = 0; i < npairs; ++i, k += 2) {
+            double* snap1 = nullptr;
+            double* snap2 = nullptr;
+            const int64_t i0 = si;
+            if (si < n_snap && snap_steps[si] == k + 1) snap1 = pool + (si++) * slice;
+            if (si < n_snap && snap_steps[si] == k + 2) snap2 = pool + (si++) * slice;
+            const bool wait = pdl && k > k0 && !(k == ka && first);
+            const bool even = (i % 2) == 0;
+            const double* uin = even ? p->u_dev[k & 1] : ps->u3;
+            double* uout = even ? ps->u3 : p->u_dev[k & 1];
+            if (int r = launch_pair(p, k, kb0, snap1, snap2, cap, wait, pdl, uin, p->u_dev[(k + 1) & 1], uout,
+                                    even ? 1 : 0, ps->step))
+                return r;
+            if (si > i0)
+                if (int r = copy_out(i0, si)) return r;
+        }
+        // the first single step after a pair must not start before it completes
+        // (its A phase reads H[k-2], which the pair wrote)
+        return steps(k, kz, kb0, first || npairs > 0);
+    };
     // the steps [ks, ke) of block kb with sub-block launches (plan->subblock)
     cudaStream_t sstream = nullptr;
     cudaEvent_t sready = nullptr, sdone[kMaxSub] = {};
@@ -2982,6 +3371,8 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
         if (overlap_enabled()) rc = side_stream(&side, &ev_fork, ev_join);
         if (rc == FG_OK && sub) rc = sub_stream(&sstream, &sready, sdone);
+        if (rc == FG_OK && pairs)
+            rc = cuda_check(cudaMemsetAsync(ps->step, 0xff, sizeof(int64_t), cap), "pair step reset");  // -1
         int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
         BlockTrace tr(graph ? nullptr : getenv("FGB200_TRACE"));
         for (int64_t kb = k0 - k0 % tb; kb < k1 && rc == FG_OK; kb += tb) {
@@ -3015,7 +3406,15 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
             rc = persistent ? persistent_steps(ks, ke, kb)
                  : chain    ? chain_steps(ks, ke, kb, start)
                  : sub      ? sub_steps(ks, ke, kb, block_len(kb), start)
+                 : pairs    ? pair_steps(ks, ke, kb, start)
                             : steps(ks, ke, kb, start);
+        }
+        if (rc == FG_OK && pairs) {  // a run that stopped on a field in the scratch buffer
+            const int64_t nf = p->B * p->ms;
+            ++g_launches;
+            fg_u3_fixup_kernel<<<(unsigned)((nf + 255) / 256 < 1024 ? (nf + 255) / 256 : 1024), 256, 0, cap>>>(
+                p->status_dev, ps->step, ps->u3, p->u_dev[0], p->u_dev[1], nf);
+            rc = cuda_check(cudaGetLastError(), "fg_u3_fixup launch");
         }
         if (main_on_side >= 0) {  // error path: never leave the side stream unjoined
             const int r2 =

@@ -457,6 +457,54 @@ def test_subblock_launch_modes_bitwise(fg, golden, name, monkeypatch):
             assert s0 == s1 and np.array_equal(a0, a1), kw
 
 
+PAIR_CASES = ["c2_small", "small", "point_full", "point_adaptive3", "point_adaptive5", "c1", "1d_adaptive",
+              "batch_adaptive", "spread_g09_adaptive4", "c2_small_full"]
+
+
+@pytest.mark.parametrize("tblock", [16, 32, 64])
+@pytest.mark.parametrize("name", PAIR_CASES)
+def test_fused_pairs_bitwise(fg, golden, name, tblock, monkeypatch):
+    kind = golden.case(name).get("strategy", [None])[0] if golden.case(name)["kind"] != "nd" else None
+    if tblock > 32 and (kind in ("full", "short") or name in ("c1", "c2_small_full", "small", "point_full")):
+        pytest.skip("factors above 32 are adaptive only")
+    """Fused step pairs (two steps per launch, halo recomputed) equal single-step
+    launches bit for bit, snapshots included; and match the reference."""
+    cfg = _any_field_config(fg, golden, name)
+    monkeypatch.setenv("FGB200_PAIRS", "0")
+    ref = fg.run_field(cfg, tblock=tblock)
+    monkeypatch.setenv("FGB200_PAIRS", "1")
+    for kw in (dict(), dict(flags=0), dict(progress_every=7), dict(flags=3)):
+        got = fg.run_field(cfg, tblock=tblock, **kw)
+        assert len(got.snapshots) == len(ref.snapshots)
+        for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
+            assert s0 == s1 and np.array_equal(a0, a1), (kw, s0)
+    test_temporal_blocking_matches_goldens(fg, golden, name, tblock)
+
+
+def test_fused_pairs_divergence(fg, golden, monkeypatch):
+    """A run that blows up reports the same first bad step and peak with and
+    without fused pairs (the bad field may sit in the pairs' scratch buffer)."""
+    u0 = np.zeros((8, 8))
+    u0[4, 4] = 10.0
+    results = set()
+    for n_steps in (500, 37, 38):
+        cfg = fg.FieldConfig(initial=u0, dx=1.0, gamma=1.0, dt=1.0, n_steps=n_steps)
+        for pairs in ("0", "1"):
+            monkeypatch.setenv("FGB200_PAIRS", pairs)
+            for tb in (16, 32):
+                try:
+                    fg.run_field(cfg, tblock=tb)
+                except fg.DivergenceError as exc:
+                    results.add((n_steps, exc.step, exc.peak))
+                else:
+                    results.add((n_steps, None, None))
+    by_n = {}
+    for n_steps, step, peak in results:
+        by_n.setdefault(n_steps, set()).add((step, peak))
+    assert all(len(v) == 1 for v in by_n.values()), by_n
+    assert next(iter(by_n[500]))[0] == golden.meta["divergence"]["step"]
+
+
 def test_wide_temporal_blocking_rejects_dense_plans(fg, golden):
     cfg = _any_field_config(fg, golden, "point_full")
     with pytest.raises(ValueError, match="tblock 64"):
