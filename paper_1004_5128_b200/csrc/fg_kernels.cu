@@ -2212,14 +2212,22 @@ BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
     const int cands[4] = {256, 224, 192, 128};
     const bool staged = p->B == 1 && p->blkcoef_dev;
     BlockVariant best = {nullptr, 0, 0};
-    int64_t best_cost = INT64_MAX;
-    for (int tp : cands) {
-        if (force && atoi(force) != tp) continue;
-        if (p->tblock == 32 && tp == 256 && !force) continue;  // spills at 32 x 256
+    auto usable = [&](int tp) { return force ? atoi(force) == tp : !(p->tblock == 32 && tp == 256); };  // 32 x 256 spills
+    auto cost_of = [&](int tp) {
         const int64_t tiles = ((p->n_m + tp - 1) / tp) * p->B;
-        const int64_t cost = ((tiles + sm_count() - 1) / sm_count()) * tp;
-        if (cost < best_cost) {
-            best_cost = cost;
+        return ((tiles + sm_count() - 1) / sm_count()) * tp;
+    };
+    int64_t min_cost = INT64_MAX;
+    for (int tp : cands)
+        if (usable(tp) && cost_of(tp) < min_cost) min_cost = cost_of(tp);
+    // the widest tile within 2 % of the best balance: a wider CTA shares its
+    // stage barrier and coefficient rows over more warps (measured c3-full at
+    // tblock 32: TP 224 705 ms vs TP 192 792 ms, nearly equal balance)
+    bool found = false;
+    for (int tp : cands) {
+        if (!usable(tp) || found) continue;
+        if (cost_of(tp) * 50 <= min_cost * 51) {
+            found = true;
             switch (p->tblock) {
                 case 8: best = block_variant_of<8>(staged, tail, tp); break;
                 case 24: best = block_variant_of<24>(staged, tail, tp); break;
