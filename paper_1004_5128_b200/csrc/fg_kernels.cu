@@ -2445,7 +2445,10 @@ int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
 
 // Item partial sums (coefficient rows already built) into Q, then the ordered
 // reduction into P (or directly into P for a single all-steps item).
-constexpr int kItemMainStages = 8;  // two main CTAs per SM: 2 x 70 KB of ring at TP 112
+#ifndef FG_ITEM_STAGES
+#define FG_ITEM_STAGES 8
+#endif
+constexpr int kItemMainStages = FG_ITEM_STAGES;  // two main CTAs per SM: 2 x 70 KB of ring at TP 112
 constexpr int kItemTailStages = 3;  // tail launches run beside the main CTAs
 
 // Item-kernel tile width: two CTAs per SM (two independent rings, so one
