@@ -2910,10 +2910,13 @@ struct GraphKey {
     int32_t flags = 0;
     std::vector<int64_t> snaps;
     std::string env;
+    std::vector<double> psi_host;  // host coefficients baked into the step launches
     GraphKey() { memset(&plan, 0, sizeof plan); }
     bool operator==(const GraphKey& o) const {
         return memcmp(&plan, &o.plan, sizeof plan) == 0 && k0 == o.k0 && k1 == o.k1 && pool == o.pool &&
-               host_pool == o.host_pool && flags == o.flags && snaps == o.snaps && env == o.env;
+               host_pool == o.host_pool && flags == o.flags && snaps == o.snaps && env == o.env &&
+               psi_host.size() == o.psi_host.size() &&
+               (psi_host.empty() || memcmp(psi_host.data(), o.psi_host.data(), psi_host.size() * sizeof(double)) == 0);
     }
 };
 
@@ -3206,6 +3209,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         key.flags = flags;
         key.snaps.assign(snap_steps, snap_steps + (n_snap > 0 ? n_snap : 0));
         key.env = graph_env();
+        if (p->psi_host && p->tblock) key.psi_host.assign(p->psi_host, p->psi_host + p->tblock + 1);
         if (gc.exec && gc.key == key) {
             g_launches += gc.kernels;
             return cuda_check(cudaGraphLaunch(gc.exec, st), "graph replay");

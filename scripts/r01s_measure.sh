@@ -3,6 +3,7 @@
 # Bench lines, ncu launch lists and full captures -> gpurun_out/r01s/.
 O=gpurun_out/r01s
 mkdir -p $O
+timeout 1800 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; echo pytest=$?
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$?
 timeout 900 python bench.py > $O/bench_default.log 2>&1; echo default=$?
 timeout 900 python bench.py --impl reference > $O/bench_ref.log 2>&1; echo ref=$?
@@ -20,5 +21,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:fg_s
 P5="python scripts/profile_run.py --config c5 --steps 1536"
 $P5 > $O/p5.log 2>&1
 timeout 1200 ncu --metrics $M --clock-control none --csv --log-file $O/c5_launches.csv $P5 > $O/ncu_l5.log 2>&1; echo l5=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fg_block_item_kernel -s 16 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:fg_block_item_kernel<.int.128, .int.8' -s 6 -c 1 \
   -o $O/c5_item16 $P5 > $O/ncu_f3.log 2>&1; echo f3=$?

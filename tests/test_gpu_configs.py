@@ -110,9 +110,11 @@ def test_c5_member_independence_bitwise(W, monkeypatch):
     import paper_1004_5128_b200 as fg
 
     cfg = W.c5(n_steps=600)
-    # same warp split, temporal block and item width in both runs (they fix the
-    # per-point summation order; the defaults differ for 2048 and 3 members)
+    # same warp split, temporal block, item width and sub-block length in both
+    # runs (they fix the per-point summation order; the defaults differ for 2048
+    # and 3 members)
     monkeypatch.setenv("FGB200_ITEM_COLS", "16")
+    monkeypatch.setenv("FGB200_SUBBLOCK", "32")
     full = fg.run_field(cfg, split=1, tblock=128).final
     idx = [5, 700, 2040]
     alone = fg.run_field(W.subset_members(cfg, idx), split=1, tblock=128).final

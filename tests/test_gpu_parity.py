@@ -505,6 +505,29 @@ def test_fused_pairs_divergence(fg, golden, monkeypatch):
     assert next(iter(by_n[500]))[0] == golden.meta["divergence"]["step"]
 
 
+def test_cached_graph_replay(fg, golden):
+    """FG_RUN_GRAPH: the second identical run replays the cached graph and
+    gives the per-step launches' bits; a different plan is re-captured."""
+    import torch
+
+    from paper_1004_5128_b200._engine import Stepper
+
+    outs = []
+    for name in ("c2_small", "point_adaptive5", "c2_small"):
+        cfg = _any_field_config(fg, golden, name)
+        ref = fg.run_field(cfg, flags=2, tblock=64).final
+        st = Stepper(cfg.to_problem(), flags=3, tblock=64, snapshots=False)
+        u0 = st.u[0].clone()
+        for _ in range(3):
+            st.reset(u0)
+            st.advance(cfg.n_steps)
+            torch.cuda.synchronize()
+            got = st.u[cfg.n_steps & 1][: st.n_m].cpu().numpy().reshape(np.asarray(ref).shape)
+            assert np.array_equal(got, ref), name
+        outs.append(got)
+    assert np.array_equal(outs[0], outs[2])
+
+
 def test_wide_temporal_blocking_rejects_dense_plans(fg, golden):
     cfg = _any_field_config(fg, golden, "point_full")
     with pytest.raises(ValueError, match="tblock 64"):
