@@ -1131,7 +1131,10 @@ template <bool STAGED>
 __host__ __device__ constexpr int ring_stages() { return STAGED ? FG_STAGED_RING : 4; }
 
 constexpr int kMainStages = FG_STAGED_RING;  // staged main launches
-constexpr int kTailStages = 2;  // tail launches: small ring, so they fit beside two main CTAs per SM
+#ifndef FG_TAIL_STAGES
+#define FG_TAIL_STAGES 2
+#endif
+constexpr int kTailStages = FG_TAIL_STAGES;  // tail launches: small ring, so they fit beside two main CTAs per SM
 
 template <int BT, int TP, bool STAGED, int NS>
 size_t tma_block_smem() {

@@ -99,3 +99,42 @@ def test_sass_is_sm100a():
     assert "LDG.E.ENL2.128" in out or "LDG.E.128" in out or re.search(r"LDG\.E[.\w]*\.128", out)
     arr = np.zeros(1)
     assert arr.size == 1
+
+
+def _valid_looking_plan():
+    """A plan whose pointers are non-NULL placeholders: validation only, never launched."""
+    plan = _lib.FgPlan()
+    plan.ndim, plan.B, plan.n_m, plan.ms = 2, 1, 64, 64
+    plan.shape[0], plan.shape[1], plan.shape[2] = 8, 8, 1
+    plan.kind, plan.base = 2, 5
+    for name in ("psi_dev", "H_dev", "status_dev", "decay_dev", "diffuse_dev", "dt_dev", "horizon_dev", "P_dev"):
+        setattr(plan, name, 8)
+    plan.u_dev[0] = plan.u_dev[1] = 8
+    plan.psi_stride = plan.h_slices = 201
+    return plan
+
+
+def test_blocking_fields_validated_without_gpu():
+    """tblock / item_cols / subblock combinations are checked before any launch
+    (a zero-step fg_run returns after validation)."""
+    L = _lib.load()
+    plan = _valid_looking_plan()
+    run = lambda: L.fg_run(C.byref(plan), 5, 5, None, 0, None, 0, None)  # noqa: E731
+    assert run() == _lib.FG_OK
+    plan.tblock = 40  # multiple of 8 above 32: adaptive with blkcoef_dev only
+    assert run() == _lib.FG_ERR_UNSUPPORTED
+    plan.blkcoef_dev = 8
+    assert run() == _lib.FG_OK
+    plan.tblock = 12
+    assert run() == _lib.FG_ERR_ARG
+    plan.tblock = 136  # above kMaxTBlock
+    assert run() == _lib.FG_ERR_ARG
+    plan.tblock = 128
+    plan.subblock = 48  # must divide tblock
+    assert run() == _lib.FG_ERR_ARG
+    plan.subblock = 4  # 32 sub-blocks > 16
+    assert run() == _lib.FG_ERR_ARG
+    plan.subblock = 32
+    assert run() == _lib.FG_OK
+    plan.kind = 0  # sub-blocks are for adaptive plans
+    assert run() in (_lib.FG_ERR_ARG, _lib.FG_ERR_UNSUPPORTED)
