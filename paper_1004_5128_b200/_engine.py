@@ -65,7 +65,7 @@ def default_tblock(p: "Problem | None" = None) -> int:
     Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
     full memory at 32 (the dense block kernel turns fp64-tensor bound);
     adaptive at 128 with 16-column items for large fields (c3, c4, c5) and at
-    64 with 8-column items otherwise (c2); short memory and other ensembles
+    56 with 8-column items otherwise (c2); short memory and other ensembles
     (per-member tables built in the CTA) at 24.
     """
     env = os.environ.get("FGB200_TBLOCK")
@@ -87,9 +87,10 @@ def default_tblock(p: "Problem | None" = None) -> int:
         return 24
     # thinned schedules: the itemized block stage does work proportional to the
     # schedule's terms, so a wider block (fewer history passes) pays off up to
-    # 64 (c2: 31.7 ms at 48, 30.2 at 64, 33.9 at 80, 36.2 at 128 — wider blocks
-    # re-read classes with more than 8 steps and lengthen the step chain)
-    return 64 if thinned else 32
+    # 56 (c2, one box: 35.8 ms at 40, 33.5 at 48, 32.7 at 56, 33.3 at 64 and 72 —
+    # at 56 the stride-7 interval has exactly 8 steps per residue class, so its
+    # 8-column items read it once; wider blocks lengthen the step chain's recent sums)
+    return 56 if thinned else 32
 
 
 def item_cols(p: "Problem") -> int:

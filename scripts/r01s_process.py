@@ -64,7 +64,8 @@ def main():
     # c2: main item launches of the launch list vs their algorithmic bytes.  Issue
     # order per block kb (fg_run_ex): main(kb + tb) on the side stream, then
     # tail(kb); main(tb) and tail(0) launch no item kernel.
-    n, tb, base, n_pts = 5000, 64, 5, 256 * 256
+    tb = int(json.load(open(os.path.join(PROF, "r01s", "bench_default.json")))["roofline"]["temporal_block"])
+    n, base, n_pts = 5000, 5, 256 * 256
     rows = [r for r in launch_rows(os.path.join(SRC, "c2_launches.csv")) if "fg_block_item8_kernel" in r["name"]]
     seq = []
     for kb in range(0, n, tb):
@@ -94,7 +95,7 @@ def main():
                     "--alg-bytes", str(alg_cap)], check=True)
     tr = json.load(open(os.path.join(PROF, "traffic.json")))
     tr["c2"]["capture"] = (f"ncu --set full --clock-control none -k regex:fg_block_item8_kernel -s 140 -c 1 python "
-                           f"scripts/profile_run.py --config c2 (tblock 64): main item launch of block kb0={kb_cap}")
+                           f"scripts/profile_run.py --config c2 (tblock {tb}): main item launch of block kb0={kb_cap}")
     tr["c2"]["kernel"] = "fg_block_item8_kernel<224, 6, false> (main)"
     tr["c2"]["launch_list_dram_over_algorithmic"] = tot_d / tot_a
     json.dump(tr, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)

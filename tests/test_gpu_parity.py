@@ -414,7 +414,7 @@ ADAPTIVE_WIDE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_a
                  "batch_adaptive", "1d_adaptive", "3d_sat_adaptive"]
 
 
-@pytest.mark.parametrize("tblock", [48, 64, 96, 128])
+@pytest.mark.parametrize("tblock", [48, 56, 64, 96, 128])
 @pytest.mark.parametrize("name", ADAPTIVE_WIDE)
 def test_wide_temporal_blocking_matches_goldens(fg, golden, name, tblock):
     """Factors above 32 (itemized main and tail launches; adaptive, single
