@@ -75,8 +75,11 @@ def default_tblock(p: "Problem | None" = None) -> int:
         return 24
     thinned = p.kind == "adaptive" and int(p.param) < int(p.n_steps)  # base >= n: the full schedule
     if thinned and large_field(p):
-        # 16-column items (see item_cols): one history pass per 128 steps
-        return 128
+        # 16-column items (see item_cols): one history pass per 112 (single
+        # field: the stride-7 interval then has exactly 16 steps per residue
+        # class; c3-adaptive 302 vs 314 ms at 128, c4-adaptive 621 vs 644) or
+        # 128 steps (ensembles: c5 1312 vs 1346 ms at 112)
+        return 128 if p.batch > 1 else 112
     if p.batch > 1:
         # ensembles: itemized (per-member coefficient rows) when thinned; dense otherwise
         return 64 if thinned else 24
@@ -117,19 +120,21 @@ def large_field(p: "Problem") -> bool:
 def default_subblock(p: "Problem", tblock: int) -> int:
     """Sub-block length S of the sub-block launches (fg_plan.subblock, 0 = off).
 
-    Large fields (c3, c4, c5) at tblock 128: the block's own slices do not fit
-    in L2, so every step re-reads its recent slices from HBM; with sub-blocks
-    each finished one is streamed once into the later steps' partial sums.
-    Measured on B200 (ms per run, S = 0 / 8 / 16 / 32): c5 1403 / 1492 / 1372 /
-    1350, c3-adaptive 335 / 423 / 339 / 323 — the steps' recent sums are bound
-    by their rounds of loads in flight more than by their count, so only the
-    longest sub-blocks pay.  FGB200_SUBBLOCK overrides (0 disables).
+    Large fields (c3, c4, c5) at tblock 112/128: the block's own slices do not
+    fit in L2, so every step re-reads its recent slices from HBM; with
+    sub-blocks each finished one is streamed once into the later steps' partial
+    sums.  Measured on B200 at tblock 128 (ms per run, S = 0 / 8 / 16 / 32 /
+    64): c5 1403 / 1492 / 1372 / 1350 / 1374, c3-adaptive 335 / 423 / 339 / 323
+    / 326 (tblock 112: S = 28 302, S = 56 312) — the steps' recent sums are
+    bound by their rounds of loads in flight more than by their count, so a
+    quarter block pays and shorter ones do not.  FGB200_SUBBLOCK overrides (0
+    disables).
     """
     env = os.environ.get("FGB200_SUBBLOCK")
     if env is not None:
         s = int(env)
     else:
-        s = 32 if large_field(p) and tblock >= 128 else 0
+        s = tblock // 4 if large_field(p) and tblock >= 112 else 0
     if s and (tblock % s or tblock // s > 16 or s < 2):
         return 0
     return s
