@@ -337,6 +337,19 @@ def check_history_budget(p: Problem) -> None:
             f"{needed} bytes, over the cap of {p.history_byte_cap}")
 
 
+_TOTALS: dict = {}
+
+
+def _device_total(device) -> int:
+    """Total device memory (cached; the properties call is cheap only once)."""
+    import torch
+
+    key = str(device)
+    if key not in _TOTALS:
+        _TOTALS[key] = int(torch.cuda.get_device_properties(device).total_memory)
+    return _TOTALS[key]
+
+
 class Stepper:
     """All device state of one run plus the loop driver."""
 
@@ -374,11 +387,15 @@ class Stepper:
             ens_rows = max(1, -(-need.value * _lib.FG_ITEM_PITCH[icols] // _lib.FG_COEF_ROW))
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         dev_bytes += 2 * B * ens_rows * _lib.FG_COEF_ROW * 8
-        free, _total = torch.cuda.mem_get_info(self.device)
-        free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
-        if dev_bytes > free:
-            raise MemoryBudgetError(
-                f"device history and fields need {dev_bytes} bytes, only {free} free on {self.device}")
+        # cudaMemGetInfo costs ~1 ms per call: ask it only when the request is
+        # not obviously small next to what torch already holds or the device has
+        idle = torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
+        if dev_bytes > idle and dev_bytes > _device_total(self.device) // 4:
+            free, _total = torch.cuda.mem_get_info(self.device)
+            free += idle
+            if dev_bytes > free:
+                raise MemoryBudgetError(
+                    f"device history and fields need {dev_bytes} bytes, only {free} free on {self.device}")
         f64 = dict(dtype=torch.float64, device=self.device)
         self.H = torch.empty((n + 1, slice_elems), **f64)
         self.u = torch.zeros((2, slice_elems), **f64)

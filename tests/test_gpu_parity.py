@@ -228,6 +228,15 @@ def test_memory_budget_enforced(fg):
         fg.run(cfg)
 
 
+def test_device_memory_checked_before_allocation(fg):
+    """A history larger than the device (1024² x 30000 steps = 252 GB, no byte
+    cap) is refused with MemoryBudgetError before anything is allocated."""
+    u0 = np.zeros((1024, 1024))
+    cfg = fg.FieldConfig(initial=u0, dx=1.0, gamma=0.5, dt=1.0, n_steps=30_000, history_byte_cap=None)
+    with pytest.raises(fg.MemoryBudgetError, match="free"):
+        fg.run_field(cfg)
+
+
 def test_progress_logging(fg, caplog):
     import logging
 
