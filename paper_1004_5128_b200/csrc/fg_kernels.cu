@@ -64,7 +64,10 @@ constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit loa
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
 constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
-constexpr int kMaxTBlock = 128;  // largest temporal-blocking factor (> 32: itemized stages only)
+#ifndef FG_MAX_TBLOCK
+#define FG_MAX_TBLOCK 128
+#endif
+constexpr int kMaxTBlock = FG_MAX_TBLOCK;  // largest temporal-blocking factor (> 32: itemized stages only)
 constexpr int kMaxSub = 16;      // most sub-blocks per temporal block (plan->subblock)
 constexpr int kMaxDenseTBlock = 32;  // largest factor of the dense block kernel
 constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxDenseTBlock + 4)
