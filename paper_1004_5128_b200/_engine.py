@@ -133,6 +133,11 @@ def default_subblock(p: "Problem", tblock: int) -> int:
     env = os.environ.get("FGB200_SUBBLOCK")
     if env is not None:
         s = int(env)
+    elif p.kind != "adaptive":
+        # dense schedules (one field): every step sums all its recent offsets,
+        # so even short sub-blocks pay (c3-short 278 -> 262 ms at S = 4,
+        # c3-full 693 -> 675 and c4-full 1414 -> 1370 at S = 8)
+        s = (8 if p.kind == "full" else 4) if large_field(p) and p.batch == 1 else 0
     else:
         s = tblock // 4 if large_field(p) and tblock >= 112 else 0
     if s and (tblock % s or tblock // s > 16 or s < 2):
@@ -470,7 +475,7 @@ class Stepper:
                 self.psi_host = np.ascontiguousarray(self.psi[0, : tb + 1].cpu().numpy())
                 plan.psi_host = self.psi_host.ctypes.data
 
-        if plan.tblock and p.kind == "adaptive" and plan.blkcoef_dev:
+        if plan.tblock and plan.blkcoef_dev and (p.kind == "adaptive" or B == 1):
             plan.subblock = default_subblock(p, int(plan.tblock))
         self.tblock = int(plan.tblock)
         self.plan = plan

@@ -1884,8 +1884,9 @@ int validate_plan(const fg_plan* p) {
     if (p->tblock && !p->P_dev) return fail(FG_ERR_ARG, "temporal blocking needs P_dev");
     if (p->subblock < 0 || (p->subblock > 0 && (!p->tblock || p->subblock < 2 || p->tblock % p->subblock != 0 ||
                                                 p->tblock / p->subblock > kMaxSub || !p->blkcoef_dev ||
-                                                p->kind != FG_MEM_ADAPTIVE)))
-        return fail(FG_ERR_ARG, "subblock must be 0, or divide tblock into at most %d parts (adaptive, blkcoef_dev)",
+                                                (p->kind != FG_MEM_ADAPTIVE && p->B != 1))))
+        return fail(FG_ERR_ARG,
+                    "subblock must be 0, or divide tblock into at most %d parts (blkcoef_dev; adaptive or one member)",
                     kMaxSub);
     if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
         FgSeg s[FG_MAX_SEGS];

@@ -136,5 +136,8 @@ def test_blocking_fields_validated_without_gpu():
     assert run() == _lib.FG_ERR_ARG
     plan.subblock = 32
     assert run() == _lib.FG_OK
-    plan.kind = 0  # sub-blocks are for adaptive plans
+    plan.kind = 0  # dense memory: single member only
+    plan.tblock, plan.subblock = 32, 8
+    assert run() == _lib.FG_OK
+    plan.B, plan.ms = 2, 64
     assert run() in (_lib.FG_ERR_ARG, _lib.FG_ERR_UNSUPPORTED)

@@ -441,27 +441,32 @@ def test_item_widths_match_goldens(fg, golden, name, cols, monkeypatch):
         test_temporal_blocking_matches_goldens(fg, golden, name, tb)
 
 
-@pytest.mark.parametrize("sub,tb", [("8", 64), ("16", 128), ("32", 128), ("8", 32)])
+@pytest.mark.parametrize("sub,tb", [("8", 64), ("16", 128), ("32", 128), ("8", 32), ("4", 24)])
 @pytest.mark.parametrize("name", ["c2_small", "point_adaptive5", "batch_adaptive", "3d_sat_adaptive",
-                                  "spread_g09_adaptive4"])
+                                  "spread_g09_adaptive4", "c2_small_full", "c2_small_short", "point_full",
+                                  "point_short100"])
 def test_subblock_launches_match_goldens(fg, golden, name, sub, tb, monkeypatch):
     """Sub-block launches (finished sub-blocks streamed into the later steps'
     partial sums on a third stream) reproduce the reference (<= 1e-10)."""
     monkeypatch.setenv("FGB200_SUBBLOCK", sub)
+    dense = name.endswith("full") or "short" in name
+    if dense and tb > 32:
+        pytest.skip("factors above 32 are adaptive only")
     test_temporal_blocking_matches_goldens(fg, golden, name, tb)
 
 
-@pytest.mark.parametrize("name", ["c2_small", "batch_adaptive"])
+@pytest.mark.parametrize("name", ["c2_small", "batch_adaptive", "c2_small_full", "c2_small_short"])
 def test_subblock_launch_modes_bitwise(fg, golden, name, monkeypatch):
     """With sub-blocks: launch modes, graph capture and split runs are bitwise equal."""
     monkeypatch.setenv("FGB200_SUBBLOCK", "8")
     cfg = _any_field_config(fg, golden, name)
-    ref = fg.run_field(cfg, flags=0, tblock=64)
+    tb = 32 if name.endswith(("_full", "_short")) else 64
+    ref = fg.run_field(cfg, flags=0, tblock=tb)
     for kw in (dict(flags=2), dict(flags=3), dict(flags=1), dict(progress_every=7), dict(progress_every=29),
                dict(flags=2, overlap="0")):
         kw = dict(kw)
         monkeypatch.setenv("FGB200_BLOCK_OVERLAP", kw.pop("overlap", "1"))
-        got = fg.run_field(cfg, tblock=64, **kw)
+        got = fg.run_field(cfg, tblock=tb, **kw)
         for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
             assert s0 == s1 and np.array_equal(a0, a1), kw
 
