@@ -45,9 +45,52 @@ class DivergenceError(RuntimeError):
     """A step produced non-finite concentrations (solver.py:38-46)."""
 
     def __init__(self, step: int, peak: float):
-        super().__init__(f"solution diverged at step {step}: max |u| reached {peak!r}")
+        # not super(): a bridged subclass (below) puts the reference's class,
+        # whose __init__ takes (step, peak), next in the MRO
+        RuntimeError.__init__(self, f"solution diverged at step {step}: max |u| reached {peak!r}")
         self.step = step
         self.peak = peak
+
+
+# The reference's callers catch the reference's own exception classes
+# (benchmark.py:114-128 records a diverging cell as a NaN row, cli.py:469-479
+# maps it to exit code 3).  When ``fracgrid`` is loaded in this process, every
+# error this package raises is an instance of BOTH its own class and the
+# reference's class of the same name, so those handlers keep working when
+# ``run`` is rebound to this package's (integrate.install).  Nothing is
+# imported: the reference module is looked up in sys.modules only.
+_REFERENCE_HOME = {
+    DivergenceError: ("fracgrid.solver", "DivergenceError"),
+    MemoryBudgetError: ("fracgrid.grid", "MemoryBudgetError"),
+    HistoryCapacityError: ("fracgrid.grid", "HistoryCapacityError"),
+}
+_BRIDGED: dict = {}
+
+
+def error_class(ours: type) -> type:
+    """``ours``, or a cached subclass of ``ours`` and the reference's same-named
+    class when that reference module is loaded (see _REFERENCE_HOME)."""
+    import sys
+
+    module, name = _REFERENCE_HOME[ours]
+    mod = sys.modules.get(module)
+    ref = getattr(mod, name, None) if mod is not None else None
+    if not isinstance(ref, type) or not issubclass(ref, BaseException) or issubclass(ours, ref):
+        return ours
+    cls = _BRIDGED.get((ours, ref))
+    if cls is None:
+        cls = type(ours.__name__, (ours, ref), {"__module__": ours.__module__, "__doc__": ours.__doc__,
+                                                "__qualname__": ours.__qualname__})
+        _BRIDGED[(ours, ref)] = cls
+    return cls
+
+
+def divergence(step: int, peak: float) -> DivergenceError:
+    return error_class(DivergenceError)(step, peak)
+
+
+def budget_error(msg: str) -> MemoryBudgetError:
+    return error_class(MemoryBudgetError)(msg)
 
 
 def default_flags() -> int:
@@ -143,6 +186,15 @@ def default_subblock(p: "Problem", tblock: int) -> int:
     if s and (tblock % s or tblock // s > 16 or s < 2):
         return 0
     return s
+
+
+def single_coef_rows(tblock: int, n_steps: int) -> int:
+    """Coefficient rows per block of a single-member blocked run (fg_plan.coef_rows):
+    rows for the tail, every slice of the main launch and the slices two
+    strides' items share; itemized blocks re-read a dense class per 8-step item."""
+    if tblock > 32:
+        return (tblock // 8 + 2) * (n_steps + 1)
+    return 2 * (n_steps + 1) + 4 * tblock
 
 
 def round_up(n: int, m: int) -> int:
@@ -337,7 +389,7 @@ def check_history_budget(p: Problem) -> None:
     needed = (n + 1) * B * p.n_m * 8
     if p.history_byte_cap is not None and needed > p.history_byte_cap:
         members = f" x{B} members" if B > 1 else ""
-        raise MemoryBudgetError(
+        raise budget_error(
             f"history of {n + 1} fields of shape {'x'.join(map(str, shape))}{members} needs "
             f"{needed} bytes, over the cap of {p.history_byte_cap}")
 
@@ -392,6 +444,8 @@ class Stepper:
             ens_rows = max(1, -(-need.value * _lib.FG_ITEM_PITCH[icols] // _lib.FG_COEF_ROW))
         dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         dev_bytes += 2 * B * ens_rows * _lib.FG_COEF_ROW * 8
+        if tb and n > tb and B == 1:
+            dev_bytes += 2 * single_coef_rows(tb, n) * _lib.FG_COEF_ROW * 8
         # cudaMemGetInfo costs ~1 ms per call: ask it only when the request is
         # not obviously small next to what torch already holds or the device has
         idle = torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
@@ -399,9 +453,23 @@ class Stepper:
             free, _total = torch.cuda.mem_get_info(self.device)
             free += idle
             if dev_bytes > free:
-                raise MemoryBudgetError(
+                raise budget_error(
                     f"device history and fields need {dev_bytes} bytes, only {free} free on {self.device}")
         f64 = dict(dtype=torch.float64, device=self.device)
+        try:
+            self._allocate(p, shape, split, slice_elems, pool_slices, ens_rows, tb, f64)
+        except torch.cuda.OutOfMemoryError as exc:
+            # a device that is mostly taken by another process: same error type
+            # as the byte-cap refusal (grid.py:141-146), before any step runs
+            raise budget_error(f"device history and fields need {dev_bytes} bytes, more than is free on "
+                               f"{self.device} ({exc.__class__.__name__})") from None
+
+    def _allocate(self, p, shape, split, slice_elems, pool_slices, ens_rows, tb, f64) -> None:
+        """Every device buffer of the run (allocated once, before the loop) and the plan."""
+        import torch
+
+        L = self.L
+        B, n = p.batch, int(p.n_steps)
         self.H = torch.empty((n + 1, slice_elems), **f64)
         self.u = torch.zeros((2, slice_elems), **f64)
         self.psi = torch.empty((B, n + 1), **f64)
@@ -464,9 +532,7 @@ class Stepper:
             if B == 1:  # per-block coefficient rows shared by all tiles
                 # two blocks in flight; rows for the tail, every slice of the main
                 # launch and the slices two strides' items share
-                rows = 2 * (n + 1) + 4 * tb
-                if tb > 32:  # itemized only: a dense class is re-read by every 8-step item
-                    rows = (tb // 8 + 2) * (n + 1)
+                rows = single_coef_rows(tb, n)
                 self.blkcoef = torch.empty((2, rows, _lib.FG_COEF_ROW), **f64)
                 plan.blkcoef_dev = self.blkcoef.data_ptr()
                 plan.coef_rows = rows
@@ -569,7 +635,7 @@ class Stepper:
         field = self.u[bad & 1].reshape(self.p.batch, self.ms)[:, : self.n_m]
         fin = field[self.torch.isfinite(field)]
         peak = float(fin.abs().max().item()) if fin.numel() else math.inf
-        raise DivergenceError(bad, peak)
+        raise divergence(bad, peak)
 
     # -------------------------------------------------------------- results --
     def fetch_snapshots(self) -> list[tuple[int, np.ndarray]]:

@@ -28,8 +28,11 @@ from . import _lib
 from ._engine import (
     DEFAULT_HISTORY_BYTE_CAP,
     DivergenceError,
+    HistoryCapacityError,
     Problem,
     Stepper,
+    divergence,
+    error_class,
     host_scalars,
     short_horizon,
     strategy_spec,
@@ -227,10 +230,6 @@ def step(u, history: HistoryBuffer, k: int, config, table: PsiTable):
     oldest = int(np.asarray(sched.offsets)[-1])
     if oldest > table.capacity:
         raise ValueError(f"psi table covers offsets up to {table.capacity}, schedule needs {oldest}")
-    if k + 1 >= history.capacity:
-        from .grid import HistoryCapacityError
-
-        raise HistoryCapacityError(f"buffer holds {history.capacity} entries and is full")
     dev = history.device
     shape = history.field_shape
     n = int(np.prod(shape))
@@ -267,8 +266,13 @@ def step(u, history: HistoryBuffer, k: int, config, table: PsiTable):
         view = nxt[:n]
         fin = view[torch.isfinite(view)]
         peak = float(fin.abs().max().item()) if fin.numel() else math.inf
-        raise DivergenceError(bad, peak)
-    _lib.check(L.fg_stencil(C.byref(plan), nxt.data_ptr(), history.storage[k + 1].data_ptr(), st), "fg_stencil")
-    history._mark(k + 2)
+        raise divergence(bad, peak)
+    # append at len(history) after the divergence check, like HistoryBuffer.append
+    # in solver.py:222-226 (a full buffer raises only once the step is known good)
+    at = len(history)
+    if at >= history.capacity:
+        raise error_class(HistoryCapacityError)(f"buffer holds {history.capacity} entries and is full")
+    _lib.check(L.fg_stencil(C.byref(plan), nxt.data_ptr(), history.storage[at].data_ptr(), st), "fg_stencil")
+    history._mark(at + 1)
     res = nxt[:n].reshape(shape).clone()
     return res.cpu().numpy() if is_np else res

@@ -49,3 +49,62 @@ def test_comparison_records_divergence(cuda_device):
     # driver does not swallow that (only candidate cells become NaN records)
     with pytest.raises(fg.DivergenceError):
         run_comparison(cfg, (1.0,), (3.0,), (2,))
+
+
+def test_rebind_seam_reference_handler_catches_gpu_divergence(cuda_device, monkeypatch):
+    """INTEGRATION.md §1 on the GPU: with a stand-in ``fracgrid`` loaded (the
+    reference's exception classes, solver.py:38-46), ``integrate.install`` rebinds
+    the driver's ``run`` and a diverging candidate run on the GPU is caught by the
+    driver's ``except fracgrid.solver.DivergenceError`` — a NaN record, as
+    benchmark.py:114-128 does (mirror of pkg/tests/test_benchmark.py:105-124)."""
+    import math
+    import sys
+    import types
+    import warnings
+
+    import paper_1004_5128_b200 as fg
+    from paper_1004_5128_b200 import integrate
+
+    pkg = types.ModuleType("fracgrid")
+    solver = types.ModuleType("fracgrid.solver")
+    bench = types.ModuleType("fracgrid.benchmark")
+
+    class DivergenceError(RuntimeError):
+        def __init__(self, step, peak):
+            super().__init__(f"solution diverged at step {step}: max |u| reached {peak!r}")
+            self.step, self.peak = step, peak
+
+    solver.DivergenceError = DivergenceError
+    bench.run = None
+
+    def cells(configs):  # the shape of benchmark.py:106-128: failures become NaN records
+        out = []
+        for cfg in configs:
+            try:
+                res = bench.run(cfg)
+                out.append((float(np.abs(res.final.data).max()), ""))
+            except solver.DivergenceError as exc:
+                out.append((math.nan, str(exc)))
+        return out
+
+    pkg.solver, pkg.benchmark = solver, bench
+    for name, mod in (("fracgrid", pkg), ("fracgrid.solver", solver), ("fracgrid.benchmark", bench)):
+        monkeypatch.setitem(sys.modules, name, mod)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        bad = fg.SimulationConfig(gamma=1.0, alpha=1.0, beta=0.0, dt=1.0, dx=1.0, nx=8, ny=8, n_steps=500,
+                                  sources=((4, 4, 10.0),))
+    good = fg.SimulationConfig(gamma=0.5, alpha=1.0, beta=0.0, dt=1.0, dx=10.0, nx=10, ny=10, n_steps=40,
+                               sources=((5, 5, 10.0),))
+    undo = integrate.install(pkg)
+    try:
+        recs = cells([good, bad])
+    finally:
+        undo()
+    assert bench.run is None
+    assert recs[0][1] == "" and math.isfinite(recs[0][0])
+    assert math.isnan(recs[1][0])
+    with pytest.raises(fg.DivergenceError) as exc:  # the same error through the package's own class
+        fg.run(bad)
+    assert isinstance(exc.value, DivergenceError)
+    assert recs[1][1] == str(exc.value) and f"step {exc.value.step}" in recs[1][1]
