@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FGB200_ABI_VERSION 3
+#define FGB200_ABI_VERSION 4
 
 #define FG_OK 0
 #define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
@@ -103,6 +103,11 @@ typedef struct fg_plan {
                                     steps two sub-blocks on, so steps sum only
                                     offsets < 2S themselves; 0 = off              */
     int64_t coef_rows;           /* rows per blkcoef buffer (0 = h_slices)          */
+    int64_t h_alloc;             /* slices allocated at H_dev (0 = h_slices): the 16-column
+                                    itemized block stage reads whole TMA boxes of kE slices
+                                    of a strided progression, up to fg_history_pad slices
+                                    past the last one it needs (never used in a sum);
+                                    a blocked adaptive run with a smaller allocation fails */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of
@@ -199,6 +204,12 @@ int fg_run_ex(const fg_plan* plan, int64_t k0, int64_t k1,
 
 /* Stream-synchronous read of status_dev[0] (first non-finite step). */
 int fg_status(const fg_plan* plan, int64_t* first_bad_step, void* stream);
+
+/* Slices to allocate at H_dev beyond h_slices (fg_plan.h_alloc = h_slices + pad)
+ * for blocked runs of this schedule: the 16-column item stage reads TMA boxes of
+ * 8 slices of a stride-s progression, so up to 7 strides past the last slice an
+ * item needs (those rows are never summed).  Host-only. */
+int fg_history_pad(int32_t kind, int64_t n_steps, int64_t base, int64_t* pad);
 
 /* Host accounting for temporal blocking: number of distinct history slices
  * t < kb0 that the block of steps kb0..kb0+bt-1 reads (the union of their

@@ -188,6 +188,18 @@ def default_subblock(p: "Problem", tblock: int) -> int:
     return s
 
 
+def history_pad(p: "Problem", tblock: int) -> int:
+    """Slices allocated past H[n] for a blocked run (fg_history_pad): the 16-column
+    item stage reads whole TMA boxes of 8 slices of a strided progression."""
+    n = int(p.n_steps)
+    if not tblock or n <= tblock or p.kind != "adaptive" or item_cols(p) != 16:
+        return 0
+    pad = C.c_int64(0)
+    _lib.check(_lib.load().fg_history_pad(_lib.MEM_KINDS["adaptive"], n, int(p.param), C.byref(pad)),
+               "fg_history_pad")
+    return int(pad.value)
+
+
 def single_coef_rows(tblock: int, n_steps: int) -> int:
     """Coefficient rows per block of a single-member blocked run (fg_plan.coef_rows):
     rows for the tail, every slice of the main launch and the slices two
@@ -442,7 +454,8 @@ class Stepper:
             _lib.check(L.fg_block_item_rows(_lib.MEM_KINDS["adaptive"], n, tb, int(p.param), 0, icols,
                                             C.byref(need)), "fg_block_item_rows")
             ens_rows = max(1, -(-need.value * _lib.FG_ITEM_PITCH[icols] // _lib.FG_COEF_ROW))
-        dev_bytes = ((n + 1) + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
+        self.h_pad = history_pad(p, tb)
+        dev_bytes = ((n + 1) + self.h_pad + 2 + pool_slices + p_slices) * slice_elems * 8 + B * (n + 1) * 8
         dev_bytes += 2 * B * ens_rows * _lib.FG_COEF_ROW * 8
         if tb and n > tb and B == 1:
             dev_bytes += 2 * single_coef_rows(tb, n) * _lib.FG_COEF_ROW * 8
@@ -470,7 +483,7 @@ class Stepper:
 
         L = self.L
         B, n = p.batch, int(p.n_steps)
-        self.H = torch.empty((n + 1, slice_elems), **f64)
+        self.H = torch.empty((n + 1 + self.h_pad, slice_elems), **f64)
         self.u = torch.zeros((2, slice_elems), **f64)
         self.psi = torch.empty((B, n + 1), **f64)
         self.status = torch.full((2,), _lib.FG_NO_BAD_STEP, dtype=torch.int64, device=self.device)
@@ -512,6 +525,7 @@ class Stepper:
             plan.vmax, plan.km = float(p.reaction[1]), float(p.reaction[2])
         plan.H_dev = self.H.data_ptr()
         plan.h_slices = n + 1
+        plan.h_alloc = n + 1 + self.h_pad
         plan.u_dev[0] = self.u[0].data_ptr()
         plan.u_dev[1] = self.u[1].data_ptr()
         plan.status_dev = self.status.data_ptr()

@@ -24,7 +24,9 @@
 //    traffic and there is no per-step launch or tail.  Same arithmetic in every
 //    mode → bitwise-identical results.
 //  * HBM-bound (0.25 flop/B): no tensor cores; roofline = 8 bytes per term.
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point, no -lcuda)
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -1401,6 +1403,7 @@ struct BlockItem {
     int32_t first_mask;  // bit c: this item is the first (in table order) to add to step col2step[c]
     int32_t ncols;     // steps in the item (<= kItemCols); column c is step col2step[c]
     uint8_t col2step[kItemCols];
+    uint8_t map;       // 16-column kernel: its stride's tensor map in ItemMaps
 };
 
 struct ItemTable {
@@ -1410,6 +1413,15 @@ struct ItemTable {
     int32_t pitch;       // its coefficient row pitch: kItemPitch8 or kItemPitch
     uint64_t zero_mask[kMaxTBlock / 64];  // main launch: steps no item touches (their P rows are zeroed)
     BlockItem it[kMaxItems];
+};
+
+// 16-column item kernel: one TMA tensor map per distinct item stride s, a 4-D
+// view [J][s][chunks][16] of the history (dims innermost first: 16 points,
+// B·ms/16 chunks of 128 bytes, residue t mod s, j = t div s), box {16, C, 1, kE}
+// with the 128-byte swizzle.  Built on the host per launch (encode_item_maps).
+constexpr int kMaxMaps = 16;
+struct ItemMaps {
+    CUtensorMap map[kMaxMaps];
 };
 
 // Coefficient rows of every item: row (coef_row + j), column c =
@@ -1623,35 +1635,99 @@ size_t item8_block_smem() {
            (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
 }
 
-// One CTA per SM walks its tiles, and per tile every item in table order,
-// through one TMA ring (the ring of fg_block_tma_kernel with staged coefficient
-// rows; the pipeline does not drain between items or tiles): an item's slices
-// are t_first + j*stride, and its partial sums are flushed from the
+// One CTA walks its tiles, and per tile every item in table order, through one
+// TMA ring (the pipeline does not drain between items or tiles): an item's
+// slices are t_first + j*stride, and its partial sums are flushed from the
 // accumulators when its last stage is done.  An item has up to 16 step columns
 // (two DMMA M tiles), so a residue class of up to 16 steps is streamed once; a
-// warp owns 16 points of the tile (two N tiles), which keeps the accumulators
-// at 8 doubles per thread — TP/16 consumer warps + 1 producer warp, <= 64
-// registers, two CTAs per SM (measured: one CTA of 14 warps per SM streamed at
-// half the rate, its item flushes stalling the SM's only ring), and two step
-// CTAs still fit beside them.  Items of at most 8 columns issue only the first
-// M tile (warp-uniform branch).
+// warp owns 16 points of the tile (one 128-byte chunk, two N tiles), which keeps
+// the accumulators at 8 doubles per thread — TP/16 consumer warps + 1 producer
+// warp, <= 64 registers, two CTAs per SM (two step CTAs still fit beside them).
+// Items of at most 8 columns issue only the first M tile (warp-uniform branch).
+//
+// A stage (kE slices of the item's progression × TP points) is ONE tensor copy
+// per box (cp.async.bulk.tensor.4d, SASS UTMALDG) from a 4-D view of the
+// history [J][s][chunks][16] for the item's stride s (ItemMaps): coordinates
+// (0, chunk, t mod s, t div s) select kE slices t, t+s, … at once.  The per-row
+// bulk copies this replaces (one UBLKCP per slice row, issued through a
+// serialised uniform loop) left the producer warp issue-bound and the DRAM
+// stream at 38 % of peak (profiles/r02_c3a_item16_*).  The box lands densely in
+// shared memory with the 128-byte swizzle: line L (128 B = one warp's 16 points
+// of one slice) has its 16-byte units XORed with L mod 8, so a B-fragment load
+// (4 slices × 8 points) splits 2 + 2 over the two bank halves — the minimum of
+// two wavefronts for 32 × 8 bytes.  That needs C chunks per box with C·fk
+// mod 8 ∈ {0, 6, 4, 2} or {0, 4, 0, 4}: boxes of 6 chunks (TP 96) or two boxes
+// of 4 chunks (TP 128).
 // ENS: ensembles (tpm tiles per member, per-member coefficient rows); the
 // single-member variant keeps the simpler addressing.
 template <int TP>
-constexpr int item_threads() { return TP / 16 * 32 + 32; }
+__host__ __device__ constexpr int item_threads() { return TP / 16 * 32 + 32; }
+template <int TP>
+__host__ __device__ constexpr int item_box_chunks() { return TP == 96 ? 6 : 4; }  // 16-point chunks per TMA box
+template <int TP>
+__host__ __device__ constexpr int item_stage_bytes() { return kE * TP * (int)sizeof(double); }  // multiple of 1024 (swizzle atom)
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// One ring stage of an item with MTE live M tiles, B fragments at the
+// swizzled byte offsets boff[ks][j] of the stage (see fg_block_item_kernel).
+template <int MTE, int MT, int NT, int CP>
+__device__ __forceinline__ void item_stage_sw(double (&d)[MT][NT][2], const double* cs, const unsigned char* rs,
+                                              const int (&boff)[kE / 4][NT], int nr, int fk, int lane,
+                                              uint64_t* empty_s, double* sink_w) {
+    double af[kE / 4][MTE], bf[kE / 4][NT];
+    uint32_t xr = 0;
+#pragma unroll
+    for (int ks = 0; ks < kE / 4; ++ks) {
+        const int e = ks * 4 + fk;
+#pragma unroll
+        for (int i = 0; i < MTE; ++i) {
+            af[ks][i] = e < nr ? cs[e * CP + 8 * i] : 0.0;
+            const unsigned long long w = (unsigned long long)__double_as_longlong(af[ks][i]);
+            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            // rows past the item's end hold other slices (or unwritten ones): masked
+            bf[ks][j] = e < nr ? *reinterpret_cast<const double*>(rs + boff[ks][j]) : 0.0;
+            const unsigned long long w = (unsigned long long)__double_as_longlong(bf[ks][j]);
+            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
+        }
+    }
+    xr = __reduce_xor_sync(0xffffffffu, xr);
+    if (lane == 0) mbar_arrive_after(empty_s, (double)xr, sink_w);
+#pragma unroll
+    for (int ks = 0; ks < kE / 4; ++ks)
+#pragma unroll
+        for (int i = 0; i < MTE; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
+}
 
 template <int TP, int NS, bool ENS>
 __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside two of these per SM
-    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
+    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T, const __grid_constant__ ItemMaps M) {
     constexpr int kStages = NS;
-    constexpr int RP = row_pitch<TP>();
     constexpr int CP = kItemPitch;
     constexpr int MT = 2;
     constexpr int NT = 2;
     constexpr int NW = TP / 16;
-    extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);                        // [kStages][kE][RP]
-    double* coef = rows + kStages * kE * RP;                              // [kStages*kE][CP]
+    constexpr int C = item_box_chunks<TP>();
+    constexpr int NB = NW / C;                       // boxes per stage
+    constexpr int SB = item_stage_bytes<TP>();
+    constexpr int BOXB = C * kE * 128;               // bytes per box
+    static_assert(NB * C == NW && SB % 1024 == 0 && BOXB % 1024 == 0, "item tile / box geometry");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // swizzle-128B boxes need 1024-byte aligned destinations (1 KB of slack is allocated)
+    unsigned char* rows = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // [kStages][SB]
+    double* coef = reinterpret_cast<double*>(rows + (size_t)kStages * SB);              // [kStages*kE][CP]
     uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kE * CP);
     uint64_t* empty = full + kStages;
     double* sink = reinterpret_cast<double*>(empty + kStages);
@@ -1668,40 +1744,51 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
     }
     __syncthreads();
 
-    if (warp == NW) {  // producer warp: lane e < nr issues row e of a stage, lane kE its coefficients
-        const uint64_t pol = l2_evict_first_policy();
-        int64_t g = 0;  // stage counter over all tiles and items
-        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-            const int64_t mem = ENS ? tile / a.tpm : 0;  // ensembles: tpm tiles per member
-            const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;
-            const int64_t row_elems = (a.ms - qm) < TP ? (a.ms - qm) : TP;
-            const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
-            for (int x = 0; x < T.n_items; ++x) {
-                const BlockItem& it = T.it[x];
-                const double* src0 = a.H + mem * a.ms + qm + it.t_first * a.slice_stride;
-                const int64_t sstride = (int64_t)it.stride * a.slice_stride;
-                const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
-                for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
-                    const int s = (int)(g % kStages);
-                    const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
-                    if (lane == 0) {
+    if (warp == NW) {  // producer warp: one lane issues a stage's boxes and coefficient rows
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int64_t g = 0;  // stage counter over all tiles and items
+            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+                const int64_t mem = ENS ? tile / a.tpm : 0;  // ensembles: tpm tiles per member
+                const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;
+                const int chunk0 = (int)((mem * a.ms + qm) >> 4);
+                for (int x = 0; x < T.n_items; ++x) {
+                    const BlockItem& it = T.it[x];
+                    const CUtensorMap* map = &M.map[it.map];
+                    const int r = (int)(it.t_first % it.stride);
+                    const int j_first = (int)(it.t_first / it.stride);
+                    const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
+                    for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+                        const int s = (int)(g % kStages);
+                        const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
                         if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                        mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + (uint32_t)(nr * CP * sizeof(double)));
+                        const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
+                        mbar_expect_tx(&full[s], (uint32_t)SB + cbytes);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b)
+                            tma_load_4d(rows + (size_t)s * SB + b * BOXB, map, 0, chunk0 + b * C, r,
+                                        j_first + (int)j0, &full[s], pol);
+                        bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, cbytes, &full[s]);
                     }
-                    __syncwarp();
-                    if (lane < nr)
-                        bulk_g2s_hint(rows + ((size_t)s * kE + lane) * RP, src0 + (j0 + lane) * sstride, row_bytes,
-                                      &full[s], pol);
-                    else if (lane == kE)
-                        bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, (uint32_t)(nr * CP * sizeof(double)),
-                                 &full[s]);
                 }
-            }
-        }  // tiles
+            }  // tiles
+        }
         return;
     }
 
     const int fr = lane >> 2, fk = lane & 3;
+    // byte offsets of this lane's B fragments in a stage: slice e = 4ks + fk,
+    // point 16·warp + 8j + fr → box warp / C, line L = e·C + warp % C, 16-byte
+    // unit (4j + fr/2) XOR (L mod 8), half (fr & 1)
+    int boff[kE / 4][NT];
+#pragma unroll
+    for (int ks = 0; ks < kE / 4; ++ks)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int L = (ks * 4 + fk) * C + warp % C;
+            const int u = (4 * j + (fr >> 1)) ^ (L & 7);
+            boff[ks][j] = (warp / C) * BOXB + L * 128 + u * 16 + (fr & 1) * 8;
+        }
     double d[MT][NT][2];
     int64_t g = 0;
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
@@ -1729,21 +1816,21 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
             const int s = (int)(g % kStages);
             mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
             const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
-            const double* rs = rows + (size_t)s * kE * RP + warp * 16 + fr;
+            const unsigned char* rs = rows + (size_t)s * SB;
             const double* cs = coef + (size_t)s * kE * CP + fr;
             // warp-uniform branch per item: only the item's M tiles are issued
             // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
             if (mt > 1)
-                item_stage<2, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
+                item_stage_sw<2, MT, NT, CP>(d, cs, rs, boff, nr, fk, lane, &empty[s], sink + warp);
             else
-                item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
+                item_stage_sw<1, MT, NT, CP>(d, cs, rs, boff, nr, fk, lane, &empty[s], sink + warp);
         }
         const uint64_t keep = l2_policy_last();  // the steps read P next
         // flush into P (this CTA owns the tile, items in table order, so the
         // sum of each step is deterministic): the first item of a step stores,
-        // later ones (and every tail item) add — loads first, one round trip.
-        // A step's row can sit in another lane than in the previous item (only
-        // this warp touches these points): the warp barrier orders the accesses.
+        // later ones (and every tail item) add.  A step's row can sit in another
+        // lane than in the previous item (only this warp touches these points):
+        // the warp barrier orders the accesses.
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
@@ -1769,7 +1856,7 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
 
 template <int TP, int NS>
 size_t item_block_smem() {
-    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * kItemPitch * sizeof(double) +
+    return 1024 + (size_t)NS * item_stage_bytes<TP>() + (size_t)NS * kE * kItemPitch * sizeof(double) +
            (2 * NS) * sizeof(uint64_t) + (TP / 16) * sizeof(double);
 }
 
@@ -2465,7 +2552,7 @@ constexpr int kItemTailStages = 3;  // tail launches run beside the main CTAs
 int choose_item_tp(const fg_plan* p) {
     static const char* force = getenv("FGB200_ITEM_TP");
     if (force) return atoi(force);
-    const int cands[3] = {112, 128, 96};
+    const int cands[2] = {128, 96};  // the 16-column kernel's swizzled box geometries
     int best = 128;
     int64_t best_cost = INT64_MAX;
     for (int tp : cands) {
@@ -2509,9 +2596,67 @@ int launch_item8_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, 
     return cuda_check(cudaGetLastError(), "fg_block_item8 launch");
 }
 
-int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, int tp, cudaStream_t st,
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library
+// links the runtime statically and not libcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+int64_t history_alloc(const fg_plan* p) { return p->h_alloc > p->h_slices ? p->h_alloc : p->h_slices; }
+
+// Tensor maps of the table's strides (ItemMaps) and each item's map index.  A
+// stage box reads kE slices of the item's progression, so its last stage may
+// read up to kE - 1 strides past the item's last slice: the history allocation
+// must cover that (fg_history_pad), else the launch fails.
+int encode_item_maps(const fg_plan* p, ItemTable& T, int tp, ItemMaps& M) {
+    const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return fail(FG_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    const int64_t halloc = history_alloc(p);
+    const cuuint64_t slice_bytes = (cuuint64_t)(p->B * p->ms) * sizeof(double);
+    int strides[kMaxMaps];
+    int nm = 0;
+    for (int x = 0; x < T.n_items; ++x) {
+        BlockItem& it = T.it[x];
+        const int64_t s = it.stride;
+        const int64_t j_end = it.t_first / s + ((int64_t)(it.n_slices + kE - 1) / kE) * kE;  // boxes end (exclusive)
+        if (j_end > halloc / s)
+            return fail(FG_ERR_ARG,
+                        "history allocation of %lld slices is too small for the item stream: stride %lld reads "
+                        "up to slice %lld (allocate h_slices + fg_history_pad slices, fg_plan.h_alloc)",
+                        (long long)halloc, (long long)s, (long long)(j_end * s - 1));
+        int m = 0;
+        while (m < nm && strides[m] != (int)s) ++m;
+        if (m == nm) {
+            if (nm == kMaxMaps) return fail(FG_ERR_UNSUPPORTED, "more than %d item strides in one block", kMaxMaps);
+            strides[nm++] = (int)s;
+            const cuuint64_t dims[4] = {16, (cuuint64_t)(p->B * p->ms / 16), (cuuint64_t)s, (cuuint64_t)(halloc / s)};
+            const cuuint64_t gstride[3] = {128, slice_bytes, (cuuint64_t)s * slice_bytes};
+            const cuuint32_t box[4] = {16, (cuuint32_t)(tp == 96 ? item_box_chunks<96>() : item_box_chunks<128>()),
+                                       1, (cuuint32_t)kE};
+            const cuuint32_t estride[4] = {1, 1, 1, 1};
+            const CUresult r = enc(&M.map[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, box,
+                                   estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(FG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for stride %lld", (int)r, (long long)s);
+        }
+        it.map = (uint8_t)m;
+    }
+    return FG_OK;
+}
+
+int launch_item_sums(const fg_plan* p, const BlockArgs& a, ItemTable& T, int tp, cudaStream_t st,
                      bool tail = false) {
-    void (*kern)(const BlockArgs, const ItemTable) = nullptr;
+    void (*kern)(const BlockArgs, const ItemTable, const ItemMaps) = nullptr;
     size_t smem = 0;
     int threads = 0;
     const bool ens = p->B > 1;
@@ -2524,7 +2669,6 @@ int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, i
     threads = item_threads<TPV>();
     switch (tp) {
         case 96: FG_ITEM_PICK(96) break;
-        case 112: FG_ITEM_PICK(112) break;
         case 128: FG_ITEM_PICK(128) break;
         default: return fail(FG_ERR_ARG, "item kernel: unsupported tile width %d", tp);
     }
@@ -2540,8 +2684,10 @@ int launch_item_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, i
     const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
     const int per = e ? atoi(e) : 2;
     const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
+    ItemMaps M;
+    if (int rc = encode_item_maps(p, T, tp, M)) return rc;
     ++g_launches;
-    kern<<<(unsigned)(a.total_tiles < cap ? a.total_tiles : cap), threads, smem, st>>>(a, T);
+    kern<<<(unsigned)(a.total_tiles < cap ? a.total_tiles : cap), threads, smem, st>>>(a, T, M);
     return cuda_check(cudaGetLastError(), "fg_block_item launch");
 }
 
@@ -3561,6 +3707,23 @@ int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64
         o[3] = T.it[x].ncols;
         for (int c = 0; c < kItemCols; ++c) o[4 + c] = c < T.it[x].ncols ? T.it[x].col2step[c] : -1;
     }
+    return FG_OK;
+}
+
+int fg_history_pad(int32_t kind, int64_t n_steps, int64_t base, int64_t* pad) {
+    if (!pad || n_steps < 0 || (kind == 2 && base < 2)) return fail(FG_ERR_ARG, "fg_history_pad: bad arguments");
+    int64_t s_max = 1;  // dense window and tail: stride 1
+    if (kind == 2) {
+        // interval i >= 2 (stride 2i - 1) is sampled by some step k <= n_steps - 1
+        // once a^(i-1) + i <= k (schedule.py:120-133)
+        int64_t a_prev = base;
+        for (int64_t i = 2; a_prev + i <= n_steps - 1; ++i) {
+            s_max = 2 * i - 1;
+            if (a_prev > INT64_MAX / base) break;
+            a_prev *= base;
+        }
+    }
+    *pad = (kE - 1) * s_max;
     return FG_OK;
 }
 

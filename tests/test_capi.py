@@ -26,7 +26,7 @@ def declared_functions():
 def test_library_exists_and_loads():
     assert os.path.exists(_lib.LIB_PATH), "run __graft_entry__.build() first"
     L = _lib.load()
-    assert L.fg_abi_version() == _lib.ABI_VERSION == 3
+    assert L.fg_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_every_declared_symbol_is_exported():
@@ -141,3 +141,26 @@ def test_blocking_fields_validated_without_gpu():
     assert run() == _lib.FG_OK
     plan.B, plan.ms = 2, 64
     assert run() in (_lib.FG_ERR_ARG, _lib.FG_ERR_UNSUPPORTED)
+
+
+def test_history_pad_host():
+    """fg_history_pad: 7 strides of the largest adaptive interval any step samples
+    (schedule.py:120-133: interval i >= 2 has stride 2i - 1, first sampled at
+    k = a^(i-1) + i); dense schedules read stride-1 boxes."""
+    import ctypes as C
+
+    from paper_1004_5128_b200 import _lib
+
+    L = _lib.load()
+    out = C.c_int64(0)
+
+    def pad(kind, n, base):
+        _lib.check(L.fg_history_pad(kind, n, base, C.byref(out)))
+        return out.value
+
+    assert pad(0, 4000, 0) == 7 and pad(1, 4000, 0) == 7
+    # a = 5: i = 6 (stride 11) first at k = 5^5 + 6 = 3131 <= 3999; i = 7 needs k >= 15632
+    assert pad(2, 4000, 5) == 7 * 11 and pad(2, 10000, 5) == 7 * 11
+    assert pad(2, 3132, 5) == 7 * 11 and pad(2, 3131, 5) == 7 * 9
+    assert pad(2, 10, 100) == 7  # base beyond the run: the full schedule
+    assert L.fg_history_pad(2, 100, 1, C.byref(out)) == _lib.FG_ERR_ARG

@@ -423,7 +423,7 @@ ADAPTIVE_WIDE = ["point_adaptive3", "point_adaptive5", "c2_small", "spread_g09_a
                  "batch_adaptive", "1d_adaptive", "3d_sat_adaptive"]
 
 
-@pytest.mark.parametrize("tblock", [48, 56, 64, 96, 128])
+@pytest.mark.parametrize("tblock", [48, 56, 64, 96, 112, 128])
 @pytest.mark.parametrize("name", ADAPTIVE_WIDE)
 def test_wide_temporal_blocking_matches_goldens(fg, golden, name, tblock):
     """Factors above 32 (itemized main and tail launches; adaptive, single
@@ -441,14 +441,18 @@ def test_item_widths_match_goldens(fg, golden, name, cols, monkeypatch):
         test_temporal_blocking_matches_goldens(fg, golden, name, tb)
 
 
-@pytest.mark.parametrize("sub,tb", [("8", 64), ("16", 128), ("32", 128), ("8", 32), ("4", 24)])
+@pytest.mark.parametrize("sub,tb,cols", [("8", 64, None), ("16", 128, None), ("32", 128, None), ("8", 32, None),
+                                         ("4", 24, None), ("28", 112, "16"), ("32", 128, "16")])
 @pytest.mark.parametrize("name", ["c2_small", "point_adaptive5", "batch_adaptive", "3d_sat_adaptive",
                                   "spread_g09_adaptive4", "c2_small_full", "c2_small_short", "point_full",
                                   "point_short100"])
-def test_subblock_launches_match_goldens(fg, golden, name, sub, tb, monkeypatch):
+def test_subblock_launches_match_goldens(fg, golden, name, sub, tb, cols, monkeypatch):
     """Sub-block launches (finished sub-blocks streamed into the later steps'
-    partial sums on a third stream) reproduce the reference (<= 1e-10)."""
+    partial sums on a third stream) reproduce the reference (<= 1e-10); (28,
+    112, 16-column items) is the default of single large adaptive fields (c3, c4)."""
     monkeypatch.setenv("FGB200_SUBBLOCK", sub)
+    if cols:
+        monkeypatch.setenv("FGB200_ITEM_COLS", cols)
     dense = name.endswith("full") or "short" in name
     if dense and tb > 32:
         pytest.skip("factors above 32 are adaptive only")
