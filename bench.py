@@ -1,23 +1,30 @@
 """Benchmark: GL history terms/s of the fused B200 stepper (and the CPU reference arm).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
 
-Workload (BASELINE.json configs[1], the metric's configuration): c2 — 2D 256x256
-fractional reaction-diffusion, γ=0.8, r=0.1, f(u)=-0.1u, adaptive memory a=5,
-5000 GL steps, seeded synthetic initial field.  One benchmark *step* = one
-complete 5000-step run (every fused step kernel of the simulation).
+Workload (default ``c4``, the largest single-GPU configuration of BASELINE.json,
+configs[3]): 3D 128³ fractional reaction-diffusion (2.1M points, fp64), γ=0.7,
+r=0.05, saturating consumption f(u) = -0.5u/(0.2+u), seeded smoothed initial
+field, 4000 steps, run with full memory AND with adaptive memory (a=5) — the
+config names both.  One benchmark *step* = one complete 4000-step run of each
+(1.68e13 + 2.15e12 history terms).  ``--config`` also takes c1, c2, c3 (full,
+short and adaptive runs), c5 or a single run (c3-adaptive, c4-full, …).
 
 Metric: GL history terms/s = Σ_k len_k · N / time, whole job over
-all ranks.  ``value`` times the run with inputs resident in HBM (CUDA events on
+all ranks.  ``value`` times the runs with inputs resident in HBM (CUDA events on
 the launching stream, barrier + synchronise on both sides, max over ranks);
 ``e2e`` times the public API ``run_field`` from host arrays (H2D of u0, D2H of
-the snapshots inside the timed region).  ``roofline`` reports the fused step
-kernel against the measured HBM copy peak; ``cpu_baseline`` the C restatement of
-the reference (oracle/, OpenMP over the host's cores) on a bounded prefix sample.
+the snapshots inside the timed region).  ``roofline`` reports the dominant
+kernel (the block stage of the run with the most block-stage time: the dense
+fp64-tensor block kernel for full memory, the TMA item kernel for adaptive
+memory) against its measured peak; ``runs`` carries every run's own numbers.
+``cpu_baseline`` is the C restatement of the reference (oracle/, OpenMP over the
+host's cores) on exact prefixes of the same runs.
 
 ``--impl reference`` times that CPU reference arm alone (rank 0; other ranks exit).
-Under torchrun (N > 1) each rank runs an independently seeded member of the
-workload (weak scaling, member sharding, no data-path collective).
+Under torchrun (N > 1) every rank runs an independently seeded replica of the
+workload (weak scaling; the spatial slab split of one field is
+``paper_1004_5128_b200.sharding``).
 """
 
 from __future__ import annotations
@@ -39,9 +46,23 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GL history terms/s (grid pts × memory terms)"
 UNIT = "terms/s"
-REF_SAMPLE_STEPS = 1000       # CPU reference arm: prefix of the c2 run per timed step
-REF_WARM_STEPS = 100
-CPU_BASELINE_STEPS = 1000     # cpu_baseline sample inside our own line (rank 0, N=1)
+# workloads made of several runs of one BASELINE config (a bench step runs each once)
+GROUPS = {
+    "c4": ("c4-full", "c4-adaptive"),
+    "c3": ("c3-full", "c3-short", "c3-adaptive"),
+}
+# CPU arms: exact prefixes (steps) of each run, sized to a few seconds of
+# 16-thread C-port time per bench step; single-core figure on shorter prefixes
+REF_PREFIX = {"c1": 2000, "c2": 1000, "c3-full": 250, "c3-short": 700, "c3-adaptive": 700,
+              "c4-full": 120, "c4-adaptive": 240, "c5": 1000}
+SINGLE_PREFIX = {"c1": 500, "c2": 300, "c3-full": 80, "c3-short": 150, "c3-adaptive": 200,
+                 "c4-full": 40, "c4-adaptive": 80, "c5": 200}
+REF_WARM_STEPS = 50
+FP64_TENSOR_PEAK = 37.0e12  # DMMA m8n8k4, measured on this pool (scripts/micro/fp64_rates.cu, profiles/fp64_rates.txt)
+
+
+def runs_of(name: str) -> tuple[str, ...]:
+    return GROUPS.get(name, (name,))
 
 
 def workload(name: str, rank: int = 0):
@@ -63,6 +84,15 @@ def workload(name: str, rank: int = 0):
     else:
         raise SystemExit(f"unknown config {name}")
     return cfg, desc
+
+
+def group_desc(name: str) -> str:
+    if name == "c4":
+        return ("c4: 3D 128^3 (2.1M points, fp64), gamma=0.7, r=0.05, saturating f(u)=-0.5u/(0.2+u), "
+                "4000 steps, full memory + adaptive memory a=5 (one run of each per step)")
+    if name == "c3":
+        return "c3: 2D 1024x1024, gamma=0.6, r=0.1, 4000 steps, full + short L=500 steps + adaptive a=5"
+    return workload(name)[1]
 
 
 def load_peaks() -> tuple[float, str]:
@@ -177,6 +207,18 @@ def cpu_reference(cfg, steps: int, nthreads: int = 0):
     return terms, res["elapsed_seconds"], n
 
 
+def cpu_group(name: str, prefixes: dict, nthreads: int = 0):
+    """(terms, seconds, description) of the C port over an exact prefix of every run."""
+    terms, secs, parts = 0, 0.0, []
+    for run in runs_of(name):
+        cfg, _ = workload(run)
+        t, el, n = cpu_reference(cfg, prefixes[run], nthreads)
+        terms += t
+        secs += el
+        parts.append(f"{run} steps 0..{n - 1} of {cfg.n_steps}")
+    return terms, secs, "; ".join(parts)
+
+
 def cpu_cores() -> int:
     from oracle import fg_oracle_c as foc
 
@@ -194,28 +236,33 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def single_core(name: str) -> dict:
+    t, el, what = cpu_group(name, SINGLE_PREFIX, nthreads=1)
+    return {"value": t / el, "unit": UNIT, "cores": 1, "sample": f"exact prefixes ({what}), 1 thread"}
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    cfg, desc = workload(args.config)
-    for _ in range(args.warmup):
-        cpu_reference(cfg, REF_WARM_STEPS)
-    tot_terms, tot_time, n = 0, 0.0, 0
+    for run in runs_of(args.config):  # warm (page cache, OpenMP pool)
+        cpu_reference(workload(run)[0], REF_WARM_STEPS)
+    tot_terms, tot_time, what = 0, 0.0, ""
     for _ in range(args.steps):
-        t, el, n = cpu_reference(cfg, REF_SAMPLE_STEPS)
+        t, el, what = cpu_group(args.config, REF_PREFIX)
         tot_terms += t
         tot_time += el
     value = tot_terms / tot_time
     cores = cpu_cores()
-    sample = (f"prefix of the first {n} of {cfg.n_steps} steps of the same workload per bench step "
-              f"(exact prefix), C restatement of the reference, {cores} OpenMP threads on {cpu_model()}")
+    sample = (f"exact prefixes of the same runs per bench step ({what}), C restatement of the reference "
+              f"(oracle/fg_oracle.c), {cores} OpenMP threads on {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_time / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": group_desc(args.config), "runs": list(runs_of(args.config)), "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "single_core": single_core(args.config)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -224,8 +271,10 @@ def run_reference(args) -> None:
 # ------------------------------------------------------------------ GPU arm --
 
 def time_block_stage(st, prob, stream) -> dict:
-    """Every block-kernel launch of one run, replayed over the resident history
-    (left by the timed runs) between CUDA events on the launching stream."""
+    """Every block-stage launch pair (main + tail) of one run, replayed over the
+    resident history (left by the timed runs) between CUDA events on the
+    launching stream.  The sub-block launches of the real run (slices inside a
+    block) are not replayed and not counted."""
     import ctypes as C
 
     import torch
@@ -251,12 +300,57 @@ def time_block_stage(st, prob, stream) -> dict:
     ms = ev0.elapsed_time(ev1)
     nbytes = sum(b[2] for b in blocks)
     flops = sum(b[3] for b in blocks)
-    fp64_peak = 37.0e12  # measured DMMA m8n8k4 rate, profiles/fp64_rates.txt
     return {"launches": len(blocks), "total_ms": ms, "avg_launch_us": ms * 1e3 / len(blocks),
             "alg_bytes_per_launch": nbytes / len(blocks), "alg_bytes_total": nbytes,
-            "alg_flops_total": flops, "fp64_tflops": flops / (ms * 1e-3) / 1e12,
-            "fp64_frac": flops / (ms * 1e-3) / fp64_peak, "fp64_peak_tflops": fp64_peak / 1e12,
-            "share_of_run": None}
+            "alg_flops_per_launch": flops / len(blocks), "alg_flops_total": flops,
+            "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "fp64_tflops": flops / (ms * 1e-3) / 1e12,
+            "fp64_frac": flops / (ms * 1e-3) / FP64_TENSOR_PEAK, "share_of_run": None}
+
+
+class Run:
+    """One run of the workload: its stepper, resident u0 and accounting."""
+
+    def __init__(self, name, rank, dev, args):
+        from paper_1004_5128_b200._engine import Stepper, execution_bytes
+
+        self.name = name
+        self.cfg, self.desc = workload(name, rank)
+        self.prob = self.cfg.to_problem()
+        flags = None if args.flags is None else int(args.flags)
+        self.st = Stepper(self.prob, device=dev, split=args.split, flags=flags, tblock=args.tblock)
+        self.u0 = self.st.u[0].clone()
+        self.terms = self.prob.terms()
+        self.single_bytes, self.exec_bytes = execution_bytes(self.prob, self.st.tblock)
+        self.ms: list[float] = []
+
+    def run(self):
+        self.st.reset(self.u0)
+        self.st.advance(self.prob.n_steps)
+
+    def roofline(self, stream, peak_gbs) -> dict:
+        st, prob = self.st, self.prob
+        run_s = statistics.mean(self.ms) / 1e3
+        out = {"run": self.name, "ms_per_run": run_s * 1e3, "terms_per_run": self.terms,
+               "terms_per_s": self.terms / run_s, "temporal_block": st.tblock,
+               "algorithmic_bytes_per_run": self.exec_bytes, "single_pass_bytes_per_run": self.single_bytes,
+               "run_achieved_gbs": self.exec_bytes / run_s / 1e9,
+               "run_frac_hbm": self.exec_bytes / run_s / 1e9 / peak_gbs,
+               "single_pass_equivalent_gbs": self.single_bytes / run_s / 1e9}
+        blk = time_block_stage(st, prob, stream) if st.tblock else None
+        if blk:
+            blk["share_of_run"] = blk["total_ms"] / (run_s * 1e3)
+            item = "fg_block_item8_kernel" if int(st.plan.item_cols) == 8 else "fg_block_item_kernel"
+            if prob.kind == "adaptive":
+                blk["kernel"] = f"fg_item_coef_kernel + {item} (main + tail)"
+                blk["bound"] = "hbm"
+            else:
+                blk["kernel"] = "fg_block_coef_kernel + fg_block_tma_kernel (main + tail)"
+                # at tblock >= 24 a dense block does 2·tblock flops per 8 history bytes:
+                # past the fp64 tensor ridge (37 TF/s ÷ 6.45 TB/s ≈ 5.7 flop/B)
+                blk["bound"] = "tensor" if st.tblock * 2 / 8 > FP64_TENSOR_PEAK / (peak_gbs * 1e9) else "hbm"
+            blk["hbm_frac"] = blk["hbm_gbs"] / peak_gbs
+        out["block_stage"] = blk
+        return out
 
 
 def run_ours(args) -> None:
@@ -264,7 +358,6 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     from paper_1004_5128_b200 import _lib
-    from paper_1004_5128_b200._engine import Stepper, execution_bytes
     from paper_1004_5128_b200.problem import run_field
     from paper_1004_5128_b200.sharding import dist_env, max_over_ranks, sum_over_ranks
 
@@ -273,143 +366,135 @@ def run_ours(args) -> None:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg, desc = workload(args.config, rank)
-    prob = cfg.to_problem()
-    n_steps = prob.n_steps
-    flags = None if args.flags is None else int(args.flags)
-    st = Stepper(prob, device=dev, split=args.split, flags=flags, tblock=args.tblock)
-    u0_dev = st.u[0].clone()
-    terms = prob.terms()
-    # algorithmic bytes per run.  Single pass: history reads
-    # 8·N·len_k plus u^k read, u^{k+1} write and δ^k write (8·N each) per step.
-    # With temporal blocking (st.tblock) the algorithm as executed reads each
-    # block's union of old slices once, plus partial sums and recent slices.
-    n_pts = prob.batch * prob.n_m
-    hist_bytes = 8 * terms
-    single_bytes, exec_bytes = execution_bytes(prob, st.tblock)
+    runs = [Run(name, rank, dev, args) for name in runs_of(args.config)]
     stream = torch.cuda.current_stream(dev)
     L = _lib.load()
-
-    def one_run():
-        st.reset(u0_dev)
-        st.advance(n_steps)
+    terms = sum(r.terms for r in runs)
 
     for _ in range(args.warmup):
-        one_run()
+        for r in runs:
+            r.run()
     torch.cuda.synchronize(dev)
-    st.raise_if_diverged()
+    for r in runs:
+        r.st.raise_if_diverged()
 
     sampler = ClockSampler(gpu_id_for(local)).start()
     time.sleep(0.3)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(runs) + 1)] for _ in range(args.steps)]
     n0 = L.fg_kernel_launches()  # the library counts every kernel it launches
-    evs[0].record(stream)
     for i in range(args.steps):
-        one_run()
-        evs[i + 1].record(stream)
+        evs[i][0].record(stream)
+        for j, r in enumerate(runs):
+            r.run()
+            evs[i][j + 1].record(stream)
     torch.cuda.synchronize(dev)
     total_launches = L.fg_kernel_launches() - n0
-    launches = total_launches // args.steps
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    per_run_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    t_local = sum(per_run_ms) / 1e3
-    st.raise_if_diverged()
+    per_step_ms = []
+    for i in range(args.steps):
+        for j, r in enumerate(runs):
+            r.ms.append(evs[i][j].elapsed_time(evs[i][j + 1]))
+        per_step_ms.append(evs[i][0].elapsed_time(evs[i][-1]))
+    t_local = sum(per_step_ms) / 1e3
+    for r in runs:
+        r.st.raise_if_diverged()
     t_max = max_over_ranks(t_local, dev)
     all_terms = sum_over_ranks(float(terms) * args.steps, dev)
     value = all_terms / t_max
     ms_per_step = t_max / args.steps * 1e3
 
-    # roofline.  Whole run: bytes of the algorithm as executed ÷ device time per
-    # run (gaps between launches count).  Dominant kernel: with temporal blocking
-    # the block stage (fg_block_coef_kernel + fg_block_tma_kernel, >50% of the
-    # launch list) timed live below; without it the step kernel, i.e. the run.
+    # roofline of the dominant kernel: the block stage of the run that spends the
+    # most time in it, replayed between CUDA events on the launching stream
     peak, peak_src = load_peaks()
-    run_s = t_local / args.steps
-    run_achieved = exec_bytes / run_s / 1e9
-    tr = load_traffic(args.config)
-    blk = time_block_stage(st, prob, stream) if st.tblock else None
-    if blk:
-        blk["share_of_run"] = blk["total_ms"] / (run_s * 1e3)
-        achieved = blk["alg_bytes_per_launch"] / (blk["avg_launch_us"] * 1e-6) / 1e9
-        item = "fg_block_item8_kernel" if int(st.plan.item_cols) == 8 else "fg_block_item_kernel"
-        sub = f" + sub-block launches (S={int(st.plan.subblock)})" if int(st.plan.subblock) else ""
-        kernel = (f"block stage (per block: fg_item_coef_kernel + {item} main + tail{sub})"
-                  if prob.kind == "adaptive" else
-                  "block stage (per block: coefficient kernels + fg_block_tma_kernel main + tail)")
-        traffic = tr["dram_bytes_per_launch"][0] * blk["alg_bytes_per_launch"] / tr["algorithmic_bytes_per_launch"][0] \
-            if tr and tr.get("algorithmic_bytes_per_launch") else None
+    per_run = [r.roofline(stream, peak) for r in runs]
+    dom = max((x for x in per_run if x["block_stage"]), key=lambda x: x["block_stage"]["total_ms"], default=None)
+    if dom:
+        blk = dom["block_stage"]
+        tr = load_traffic(dom["run"])
+        traffic = None
+        if tr and tr.get("algorithmic_bytes_per_launch"):
+            # ncu DRAM bytes of the captured launch, scaled to the average launch
+            traffic = tr["dram_bytes_per_launch"][0] * blk["alg_bytes_per_launch"] / tr["algorithmic_bytes_per_launch"][0]
+        if blk["bound"] == "tensor":
+            achieved = blk["alg_flops_per_launch"] / (blk["avg_launch_us"] * 1e-6) / 1e12
+            roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK / 1e12, "unit": "TFLOP/s",
+                        "frac": achieved * 1e12 / FP64_TENSOR_PEAK, "traffic": traffic,
+                        "peak_source": "measured fp64 DMMA m8n8k4 rate on this pool (profiles/fp64_rates.txt; "
+                                       "MEASURED_PEAKS.json has no fp64 figure)",
+                        "hbm_frac": blk["hbm_frac"], "hbm_peak_gbs": peak}
+        else:
+            achieved = blk["alg_bytes_per_launch"] / (blk["avg_launch_us"] * 1e-6) / 1e9
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "traffic": traffic, "peak_source": peak_src}
+        roofline.update({"kernel": f"{dom['run']}: {blk['kernel']}", "traffic_detail": tr, "runs": per_run,
+                         "note": ("achieved = algorithmic bytes (or flops) per block-stage launch pair of the "
+                                  "dominant run / its average duration (CUDA events on the launching stream); "
+                                  "traffic = ncu DRAM bytes of a captured launch scaled by its algorithmic-byte "
+                                  "ratio.  With temporal blocking one history pass serves temporal_block steps, "
+                                  "so single_pass_equivalent_gbs exceeds the HBM peak")})
     else:
-        achieved = run_achieved
-        kernel = "fg_step_kernel"
-        traffic = tr["dram_bytes_per_launch"][0] if tr else None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_detail": tr, "kernel": kernel, "block_stage": blk,
-                "run_achieved": run_achieved, "run_frac": run_achieved / peak,
-                "peak_source": peak_src,
-                "algorithmic_bytes_per_run": exec_bytes,
-                "single_pass_bytes_per_run": single_bytes,
-                "single_pass_equivalent_gbs": single_bytes / run_s / 1e9,
-                "history_bytes_per_run": hist_bytes,
-                "launches_per_run": launches,
-                "avg_launch_us": run_s / launches * 1e6,
-                "temporal_block": st.tblock,
-                "note": ("achieved = algorithmic bytes per launch of the dominant kernel / its average launch "
-                         "time (CUDA events on the launching stream); traffic = ncu DRAM bytes of the captured "
-                         "launch scaled to the average launch by its algorithmic-byte ratio; run_achieved = "
-                         "executed algorithmic bytes per run / run time.  With temporal blocking one history "
-                         "pass serves temporal_block steps, so the single-pass-equivalent rate exceeds HBM peak")}
+        run_s = t_local / args.steps
+        ex = sum(r.exec_bytes for r in runs)
+        roofline = {"bound": "hbm", "achieved": ex / run_s / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": ex / run_s / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                    "kernel": "fg_step_kernel (whole run)", "runs": per_run}
 
-    ctas, threads, split = st.geometry()
-    h2d = st.h2d_bytes
-    d2h = 8 * prob.batch * st.ms * len([s for s in st.snap_steps if s > 0])
-    st_flags = st.flags
-    del st, u0_dev  # free the resident history before the public-API runs allocate theirs
+    launch_geo = [dict(zip(("ctas", "threads", "split"), r.st.geometry()), flags=r.st.flags) for r in runs]
+    h2d = sum(r.st.h2d_bytes for r in runs)
+    d2h = sum(8 * r.prob.batch * r.st.ms * len([s for s in r.st.snap_steps if s > 0]) for r in runs)
+    info = [{"run": r.name, "grid": list(r.prob.shape), "members": r.prob.batch, "n_steps": r.prob.n_steps,
+             "memory": f"{r.prob.kind}:{r.prob.param}" if r.prob.kind != "full" else "full",
+             "history_gb": (r.prob.n_steps + 1) * r.prob.batch * r.prob.n_m * 8 / 1e9, "terms_per_run": r.terms}
+            for r in runs]
+    cfgs = [r.cfg for r in runs]
+    flags = None if args.flags is None else int(args.flags)
+    del runs  # free the resident histories before the public-API runs allocate theirs
     torch.cuda.empty_cache()
 
-    # end to end through the public API, host arrays in and out (one untimed call
+    # end to end through the public API, host arrays in and out (one untimed pass
     # first, like the device arm's warm-up: allocator pools and pinned staging)
-    run_field(cfg, split=args.split, flags=flags, tblock=args.tblock)
+    for cfg in cfgs:
+        run_field(cfg, split=args.split, flags=flags, tblock=args.tblock)
     e2e_times = []
-    for i in range(max(1, min(args.steps, 5))):
+    for _ in range(max(1, min(args.steps, 5))):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        res = run_field(cfg, split=args.split, flags=flags, tblock=args.tblock)
-        t1 = time.perf_counter()
-        e2e_times.append(t1 - t0)
-        del res
+        for cfg in cfgs:
+            res = run_field(cfg, split=args.split, flags=flags, tblock=args.tblock)
+            del res
+        e2e_times.append(time.perf_counter() - t0)
     e2e_local = statistics.mean(e2e_times)
     e2e_max = max_over_ranks(e2e_local, dev)
     e2e_value = sum_over_ranks(float(terms), dev) / e2e_max
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t, el, n = cpu_reference(cfg, CPU_BASELINE_STEPS)
+        t, el, what = cpu_group(args.config, REF_PREFIX)
         cpu = {"value": t / el, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"first {n} of {n_steps} steps of the same workload (exact prefix), C restatement of "
-                         f"the reference path, OpenMP on {cpu_model()}"}
+               "sample": f"exact prefixes of the same runs ({what}), C restatement of the reference path "
+                         f"(oracle/fg_oracle.c), OpenMP on {cpu_model()}",
+               "single_core": single_core(args.config)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "grid": list(prob.shape), "members_per_rank": prob.batch,
-                       "n_steps": n_steps, "memory": f"{prob.kind}:{prob.param}" if prob.kind != "full" else "full",
-                       "history_gb": (n_steps + 1) * n_pts * 8 / 1e9, "terms_per_run": terms,
+            "config": {"workload": group_desc(args.config), "runs": info, "terms_per_step": terms,
                        "l2": "inputs larger than L2 (history > 126 MB L2; not flushed)",
-                       "parallelism": f"member-sharded x{world}" if world > 1 else "single GPU",
-                       "launch": {"ctas": ctas, "threads": threads, "split": split, "flags": st_flags}},
+                       "parallelism": f"independent replicas x{world} (weak scaling)" if world > 1 else "single GPU",
+                       "launch": launch_geo},
             "gpu_launches": total_launches,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_max},
             "clocks": clocks,
-            "per_run_ms": per_run_ms,
+            "per_step_ms": per_step_ms,
             "device": torch.cuda.get_device_name(dev),
         }
         print(json.dumps(line), flush=True)
@@ -423,7 +508,7 @@ def main(argv=None) -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--flags", type=int, default=None)
     ap.add_argument("--tblock", type=int, default=None, help="temporal blocking factor (0 = off)")
