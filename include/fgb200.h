@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FGB200_ABI_VERSION 4
+#define FGB200_ABI_VERSION 5
 
 #define FG_OK 0
 #define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
@@ -49,8 +49,9 @@ enum fg_reaction {
 
 /*
  * Everything one run needs, as plain device pointers and sizes.  The caller
- * (Python host, or any C program) owns every buffer; the library never allocates
- * device memory.  Layout in HBM:
+ * (Python host, or any C program) owns every device buffer of a run, scratch
+ * included; the library allocates none (it keeps only per-thread streams and
+ * events for its side-stream pipelines).  Layout in HBM:
  *   fields   u[2][B][ms]                      fp64, ping-pong by step parity
  *   history  H[h_slices][B][ms]               fp64, slice t = δ^t = stencil(u^t)
  *   ψ        psi[B][psi_stride]               fp64, ψ_b(m), m = 0..n_steps
@@ -108,6 +109,9 @@ typedef struct fg_plan {
                                     of a strided progression, up to fg_history_pad slices
                                     past the last one it needs (never used in a sum);
                                     a blocked adaptive run with a smaller allocation fails */
+    double* pair_dev;            /* [B*ms + 1] caller scratch of fused step pairs (1D/2D
+                                    blocked runs): a field buffer, then the int64 step
+                                    whose field it holds; NULL disables pairs       */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of
@@ -176,15 +180,18 @@ int fg_step(const fg_plan* plan, int64_t k, double* snap_dev, void* stream);
  * All modes produce bitwise-identical results.  With temporal blocking the
  * per-step modes run each block's main block-kernel launch on a library-owned
  * low-priority side stream, forked from and joined back into `stream` inside
- * the call (FGB200_BLOCK_OVERLAP=0 disables it; results are unchanged). */
+ * the call (FG_RUN_NO_OVERLAP keeps them on `stream`; results are unchanged). */
 #define FG_RUN_GRAPH 1
 #define FG_RUN_PDL 2
 #define FG_RUN_PERSISTENT 4
-/* Temporal blocking: one launch per block whose CTAs (one per tile) wait only
- * for the tiles their stencil reads, one step apart (no grid barrier, no
- * per-step launch); used when every tile's CTA fits on the GPU at once, else
- * per-step launches.  Results are bitwise identical to the other modes. */
-#define FG_RUN_CHAIN 32
+/* Launch-shape options (results are bitwise identical either way):
+ *   FG_RUN_NO_OVERLAP  main block-stage launches on `stream`, no side stream;
+ *   FG_RUN_NO_PAIRS    no fused step pairs;
+ *   FG_RUN_PAIRS       fused step pairs for 2D fields too (default: 1D only);
+ *                      pairs need plan->pair_dev. */
+#define FG_RUN_NO_OVERLAP 64
+#define FG_RUN_NO_PAIRS 128
+#define FG_RUN_PAIRS 256
 /* Temporal blocking: P_dev already holds the partial sums of the block that
  * contains k0 (this call continues the previous fg_run of the same plan), so a
  * block that started before k0 is not recomputed. */

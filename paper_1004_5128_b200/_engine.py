@@ -102,6 +102,22 @@ def default_flags() -> int:
     return _lib.FG_RUN_PDL
 
 
+def env_flags() -> int:
+    """Launch-shape options from the environment, read per call (tests toggle them);
+    results are bitwise identical either way: FGB200_BLOCK_OVERLAP=0 (no side
+    stream for the main block-stage launches), FGB200_PAIRS=0/1 (fused step
+    pairs off / also in 2D)."""
+    f = 0
+    if os.environ.get("FGB200_BLOCK_OVERLAP") == "0":
+        f |= _lib.FG_RUN_NO_OVERLAP
+    pairs = os.environ.get("FGB200_PAIRS")
+    if pairs == "0":
+        f |= _lib.FG_RUN_NO_PAIRS
+    elif pairs == "1":
+        f |= _lib.FG_RUN_PAIRS
+    return f
+
+
 def default_tblock(p: "Problem | None" = None) -> int:
     """Temporal blocking factor (0 = off): one history pass feeds this many steps.
 
@@ -459,6 +475,9 @@ class Stepper:
         dev_bytes += 2 * B * ens_rows * _lib.FG_COEF_ROW * 8
         if tb and n > tb and B == 1:
             dev_bytes += 2 * single_coef_rows(tb, n) * _lib.FG_COEF_ROW * 8
+        self.pairs_possible = bool(tb and n > tb and len(shape) <= 2 and p.kind != "short")
+        if self.pairs_possible:
+            dev_bytes += (slice_elems + 1) * 8
         # cudaMemGetInfo costs ~1 ms per call: ask it only when the request is
         # not obviously small next to what torch already holds or the device has
         idle = torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
@@ -533,6 +552,9 @@ class Stepper:
         plan.horizon_max = max(hz) if p.kind == "short" else 0
         plan.item_cols = item_cols(p)
         self.P = None
+        if self.pairs_possible:  # fused step pairs: u^{k+2} buffer + the step it holds
+            self.pair = torch.empty(slice_elems + 1, **f64)
+            plan.pair_dev = self.pair.data_ptr()
         if tb and n > tb:
             # two buffers: block j's steps read one while block j+1's main launch
             # fills the other (fg_run's side-stream pipeline)
@@ -603,7 +625,7 @@ class Stepper:
                 self.pool_host = self.torch.empty(self.pool.shape, dtype=self.torch.float64, pin_memory=True)
             host = self.pool_host.data_ptr()
             self.copied.update(i for i, s in enumerate(snaps) if k0 < s <= k1)
-        fl = self.flags if flags is None else flags
+        fl = (self.flags if flags is None else flags) | env_flags()
         _lib.check(self.L.fg_run_ex(C.byref(self.plan), k0, k1, arr, len(snaps), pool, host,
                                     fl | self._continue_flag(k0), _lib.stream_handle()), "fg_run_ex")
         if self.tblock:

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FGB200_LIB") or os.path.join(HERE, "_lib", "libfgb200.so")
 
-ABI_VERSION = 4  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
+ABI_VERSION = 5  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
 FG_OK = 0
 FG_ERR_ARG = -1
 FG_ERR_CUDA = -2
@@ -21,7 +21,9 @@ FG_NO_BAD_STEP = (1 << 63) - 1
 FG_RUN_GRAPH = 1
 FG_RUN_PDL = 2
 FG_RUN_PERSISTENT = 4
-FG_RUN_CHAIN = 32
+FG_RUN_NO_OVERLAP = 64
+FG_RUN_NO_PAIRS = 128
+FG_RUN_PAIRS = 256
 FG_RUN_CONTINUE = 16
 FG_STEP_M0_FROM_HISTORY = 1
 FG_COEF_ROW = 36  # doubles per coefficient row of blkcoef_dev (include/fgb200.h)
@@ -80,6 +82,7 @@ class FgPlan(C.Structure):
         ("subblock", C.c_int64),
         ("coef_rows", C.c_int64),
         ("h_alloc", C.c_int64),
+        ("pair_dev", C.c_void_p),
     ]
 
 

@@ -147,46 +147,6 @@ __device__ __forceinline__ void grid_wait(const unsigned long long* bar, unsigne
     __syncthreads();
 }
 
-// Chain launches (FG_RUN_CHAIN, opt-in).  Measured on B200 (c2): 4.2 µs per
-// step with the recent sum disabled and no concurrent block stage, vs 4.0 µs
-// for PDL per-step launches *with* it — the flag hand-off (release drain +
-// acquire poll through L2) costs about what a kernel boundary does, and the A
-// phase no longer overlaps the previous step; so PDL stays the default.
-// Tile t may start step k once (1) every tile its stencil
-// reads (same member, |i - j| <= dep) has finished step k-1 — their u^k is
-// written and their reads of u^{k-1}, whose buffer step k overwrites, are
-// done — and (2) every tile has finished step k-2.  (2) bounds the drift to
-// one step, so a non-finite value raised at step s-1 stops every tile before
-// step s+1 and u^s stays intact for the divergence report, exactly as in the
-// lockstep modes; it costs nothing while (1) is the tighter condition.
-// flags[t] = steps of this launch tile t has finished; bar = their sum.
-__device__ __forceinline__ void chain_wait(const unsigned long long* flags, const unsigned long long* bar, int tile,
-                                           int tpm, int dep, unsigned long long need, unsigned long long grid) {
-    // the acquire loads order this warp's later reads; bar.sync extends that to
-    // the CTA (no separate fence: a gpu-scope fence costs a full drain)
-    if (threadIdx.x < 32) {
-        const int first = (tile / tpm) * tpm, i = tile - first;
-        const int lo = i - dep > 0 ? i - dep : 0, hi = i + dep < tpm - 1 ? i + dep : tpm - 1;
-        for (int d = lo + (int)threadIdx.x; d <= hi; d += 32)
-            while (ld_acquire(flags + first + d) < need) {
-            }
-        if (threadIdx.x == 0 && need >= 2)
-            while (ld_acquire(bar) < (need - 1) * grid) {
-            }
-    }
-    __syncthreads();
-}
-
-// Publish `done` finished steps of this tile (all threads' stores first).
-__device__ __forceinline__ void chain_arrive(unsigned long long* flags, unsigned long long* bar, int tile,
-                                             unsigned long long done, unsigned long long add) {
-    __syncthreads();
-    if (threadIdx.x == 0) {  // release is cumulative over the CTA's stores ordered by bar.sync
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + tile), "l"(done) : "memory");
-        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(bar), "l"(add) : "memory");
-    }
-}
-
 // ------------------------------------------------------------------- stencil ---
 // grid.py:98-105 operation order, each op correctly rounded (no contraction):
 //   2D ((((x+ + x-) - 4c) + y+) + y-); 1D (x+ + x-) - 2c; 3D with -6c, y±, z±.
@@ -353,27 +313,6 @@ struct StepArgs {
     // no ψ loads and no conversions on its critical path
     int32_t has_rc;
     double rc0, rc1;
-    double rc[kMaxTBlock];
-    // chain launches (FG_RUN_CHAIN): one launch per temporal block, one CTA per
-    // tile, no grid barrier — a tile waits only for the tiles its stencil reads
-    // (flags) and, one step behind, for the whole grid (bar), see chain_wait
-    const struct RecentRow* rtab;  // [bt] recent lists of the block's steps (device)
-    unsigned long long* flags;      // [total_tiles] steps done in this launch, per tile
-    int32_t chain;
-    int32_t dep;                    // stencil reach in tiles (within a member)
-    int32_t n_csnap;                // chain: snapshots taken in this launch (<= kChainSnaps)
-    int32_t csnap_slot[8];          //   their pool slots
-    int64_t csnap_step[8];          //   and the step they record (u^{k+1} of step k)
-};
-constexpr int kChainSnaps = 8;
-
-// Recent list of one blocked step in device memory (chain launches): what the
-// single-step launches get as parameters (recent_list + host coefficients).
-struct RecentRow {
-    int32_t rn, rw1;
-    double rc0, rc1;
-    uint8_t rm[kMaxTBlock];
-    uint8_t rwt[kMaxTBlock];
     double rc[kMaxTBlock];
 };
 
@@ -572,14 +511,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
             const double* rcoef = a.has_rc ? a.rc : nullptr;
             int rn = a.rn;
             w1 = a.rw1;
-            if (multi && a.rtab) {  // chain launches: the block's table (fg_recent_table_kernel)
-                const RecentRow& row = a.rtab[bb];
-                rm = row.rm;
-                rwt = row.rwt;
-                rcoef = a.has_rc ? row.rc : nullptr;
-                rn = row.rn;
-                w1 = row.rw1;
-            } else if (multi) {
+            if (multi) {
                 if (tid == 0) s_rn = recent_list(a.kind, k, a.kb0, a.base, a.hz_max, s_rm, s_rwt, &s_w1);
                 __syncthreads();
                 rm = s_rm;
@@ -643,11 +575,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
         }
 
         // ================= dependency on step k-1 =================
-        if (a.chain) {
-            if (k > a.k0)
-                chain_wait(a.flags, a.bar, blockIdx.x, a.tpm, a.dep, (unsigned long long)(k - a.k0),
-                           (unsigned long long)G);
-        } else if (multi) {
+        if (multi) {
             if (k > a.k0) grid_wait(a.bar, (unsigned long long)(k - a.k0) * (unsigned long long)G);
         } else {
             if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -670,10 +598,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
         if (a.snap_slot) {  // persistent launches: snapshot slot of step k+1 from the map
             const int32_t sl = a.snap_slot[k + 1];
             snap = sl >= 0 ? a.pool + (int64_t)sl * a.slice_stride : nullptr;
-        } else if (a.chain) {
-            snap = nullptr;
-            for (int i = 0; i < a.n_csnap; ++i)
-                if (a.csnap_step[i] == k + 1) snap = a.pool + (int64_t)a.csnap_slot[i] * a.slice_stride;
         }
         if (split == 0) {
             for (int p = 0; p < a.passes; ++p) {
@@ -711,13 +635,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                     acc0 = __dadd_rn(acc0, pb.x);
                     acc1 = __dadd_rn(acc1, pb.y);
                 }
-                const bool host_c = BLK && a.has_rc && (!multi || a.rtab);  // single-member coefficients, precomputed
+                const bool host_c = BLK && a.has_rc && !multi;  // single-member coefficients, precomputed
                 if (m1) {
-                    const double c1 = host_c ? (a.rtab ? a.rtab[bb].rc1 : a.rc1) : __dmul_rn((double)w1, __ldg(psi_b + 1));
+                    const double c1 = host_c ? a.rc1 : __dmul_rn((double)w1, __ldg(psi_b + 1));
                     acc0 = fma(c1, h1.x, acc0);
                     acc1 = fma(c1, h1.y, acc1);
                 }
-                const double c0 = host_c ? (a.rtab ? a.rtab[bb].rc0 : a.rc0) : __ldg(psi_b);  // w_0 * ψ(0) = 1 * 1
+                const double c0 = host_c ? a.rc0 : __ldg(psi_b);  // w_0 * ψ(0) = 1 * 1
                 acc0 = fma(c0, d0, acc0);
                 acc1 = fma(c0, d1, acc1);
 
@@ -745,13 +669,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 if (snap) st_pair_hint(snap + moff, n0, n1, drop);
             }
         }
-        if (!live) {  // uniform: every thread read the same flag
-            // chain: release every tile that could still wait on this one
-            if (a.chain) chain_arrive(a.flags, a.bar, blockIdx.x, ~0ull >> 2, (unsigned long long)(a.k1 - k));
-            return;
-        }
-        if (a.chain) chain_arrive(a.flags, a.bar, blockIdx.x, (unsigned long long)(k - a.k0 + 1), 1ull);
-        else if (multi) grid_arrive(a.bar);
+        if (!live) return;  // uniform: every thread read the same flag
+        if (multi) grid_arrive(a.bar);
     }
 }
 
@@ -772,6 +691,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
 // scratch buffer and the parity buffer u[k & 1], and run in even numbers so the
 // field is back in its parity buffer after each sequence.  *u3_step records
 // which step's field sits in the scratch buffer (fg_u3_fixup_kernel).
+// Recent list of one blocked step (the pair kernel's second step).
+struct RecentRow {
+    int32_t rn, rw1;
+    double rc0, rc1;
+    uint8_t rm[kMaxTBlock];
+    uint8_t rwt[kMaxTBlock];
+    double rc[kMaxTBlock];
+};
+
 struct PairArgs {
     StepArgs s;                // step k: shared fields, recent list, P (block kb0)
     RecentRow r2;              // step k+1's recent list
@@ -1000,22 +928,6 @@ __global__ void fg_u3_fixup_kernel(const int64_t* status, const int64_t* u3_step
         dst[i] = u3[i];
 }
 
-// Recent lists of the steps kb0 .. kb0+bt-1 of a block for chain launches (one
-// thread per step; single member: coefficients w·ψ(m) rounded once, as the host
-// computes them for single-step launches).
-__global__ void fg_recent_table_kernel(RecentRow* __restrict__ tab, int kind, int64_t kb0, int bt, int64_t base,
-                                       int64_t hz, const double* __restrict__ psi, int with_coef) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= bt) return;
-    RecentRow& r = tab[b];
-    r.rn = recent_list(kind, kb0 + b, kb0, base, hz, r.rm, r.rwt, &r.rw1);
-    if (with_coef) {
-        for (int e = 0; e < r.rn; ++e) r.rc[e] = __dmul_rn((double)r.rwt[e], psi[r.rm[e]]);
-        r.rc1 = __dmul_rn((double)r.rw1, psi[1]);
-        r.rc0 = psi[0];
-    }
-}
-
 // ------------------------------------------------------- temporal blocking ---
 // fg_block_tma_kernel: one pass over the history slices t < kb0 feeds the old
 // part of the next `bt` steps (kb0 .. kb0+bt-1) at once:
@@ -1067,10 +979,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-
 // Release a ring slot only once the warp's tensor-core work on it has consumed
 // its shared-memory operands: the fake `dep` input (a result of the warp's last
 // DMMA) makes the arrive wait for that DMMA, hence for every LDS feeding the
@@ -1083,6 +991,12 @@ __device__ __forceinline__ void mbar_arrive_after(uint64_t* b, double dep, doubl
         "mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)),
         "d"(dep), "r"(smem_u32(sink))
         : "memory");
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
@@ -1281,6 +1195,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     const double* psi_b = a.psi + mem * a.psi_stride;
     const int ngroups = TP / BT;  // threads per step column when filling the table
     int64_t g = 0;
+    const uint32_t rows_s = smem_u32(rows) + (uint32_t)((warp * 32 + fr) * 8), coef_s = smem_u32(coef) + (uint32_t)(fr * 8);
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
     const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
     double d[MT][NT][2];
@@ -1288,6 +1203,7 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    uint64_t* pend = nullptr;  // slot of the previous stage, released by the next one
     for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
         const int64_t t0 = ts + gl * kE;
         if (!staged && (gl * kE) % kCH == 0) {
@@ -1318,33 +1234,24 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
         const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
-        const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
-        const double* cs = (staged ? coef + (size_t)s * kE * CP : coef + ((gl * kE) % kCH) * CP) + fr;
-        // all fragments of the stage into registers first ...
+        const uint32_t rs = rows_s + (uint32_t)(s * kE * RP * 8);
+        const uint32_t cs = staged ? coef_s + (uint32_t)(s * kE * CP * 8) : coef_s + (uint32_t)(((gl * kE) % kCH) * CP * 8);
+        // all fragments of the stage into registers first (partial last stage masked) ...
         double af[kE / 4][MT], bf[kE / 4][NT];
-        uint32_t x = 0;
 #pragma unroll
         for (int ks = 0; ks < kE / 4; ++ks) {
             const int e = ks * 4 + fk;
 #pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                af[ks][i] = e < nr ? cs[e * CP + 8 * i] : 0.0;
-                const unsigned long long w = (unsigned long long)__double_as_longlong(af[ks][i]);
-                x ^= (uint32_t)w ^ (uint32_t)(w >> 32);
-            }
+            for (int i = 0; i < MT; ++i) af[ks][i] = e < nr ? lds_f64(cs + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                bf[ks][j] = e < nr ? rs[e * RP + 8 * j] : 0.0;  // partial last stage
-                const unsigned long long w = (unsigned long long)__double_as_longlong(bf[ks][j]);
-                x ^= (uint32_t)w ^ (uint32_t)(w >> 32);
-            }
+            for (int j = 0; j < NT; ++j) bf[ks][j] = e < nr ? lds_f64(rs + (uint32_t)((e * RP + 8 * j) * 8)) : 0.0;
         }
-        // ... then release the slot: the warp-wide xor of every lane's loaded
-        // values makes the arrive wait until all of this warp's shared-memory
-        // reads of the slot have returned (ptxas otherwise issues the arrive right
-        // after the loads are *issued*, racing the producer's next bulk copy).
-        x = __reduce_xor_sync(0xffffffffu, x);
-        if (lane == 0) mbar_arrive_after(&empty[s], (double)x, sink + warp);
+        // ... then release the PREVIOUS stage's slot: the release depends on that
+        // stage's last DMMA result, and that DMMA (like every one before it) only
+        // issued once the fragments it read from the slot were in registers —
+        // so the producer's next bulk copy cannot overwrite rows still being read
+        if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1], sink + warp);
+        pend = &empty[s];
 #pragma unroll
         for (int ks = 0; ks < kE / 4; ++ks)
 #pragma unroll
@@ -1352,6 +1259,8 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
 #pragma unroll
                 for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
     }
+    // the tile's last stage: released once its DMMAs are done (the flush needs them anyway)
+    if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1], sink + warp);
     // D fragment: row = step fr (+8 per M tile), columns = 2 adjacent points
     double* pout = a.P + mem * a.ms + q0 + warp * 32 + fk * 2;
 #pragma unroll
@@ -1645,10 +1554,10 @@ size_t item8_block_smem() {
 // warp, <= 64 registers, two CTAs per SM (two step CTAs still fit beside them).
 // Items of at most 8 columns issue only the first M tile (warp-uniform branch).
 //
-// A stage (kE slices of the item's progression × TP points) is ONE tensor copy
+// A stage (kIR slices of the item's progression × TP points) is ONE tensor copy
 // per box (cp.async.bulk.tensor.4d, SASS UTMALDG) from a 4-D view of the
 // history [J][s][chunks][16] for the item's stride s (ItemMaps): coordinates
-// (0, chunk, t mod s, t div s) select kE slices t, t+s, … at once.  The per-row
+// (0, chunk, t mod s, t div s) select kIR slices t, t+s, … at once.  The per-row
 // bulk copies this replaces (one UBLKCP per slice row, issued through a
 // serialised uniform loop) left the producer warp issue-bound and the DRAM
 // stream at 38 % of peak (profiles/r02_c3a_item16_*).  The box lands densely in
@@ -1660,12 +1569,18 @@ size_t item8_block_smem() {
 // of 4 chunks (TP 128).
 // ENS: ensembles (tpm tiles per member, per-member coefficient rows); the
 // single-member variant keeps the simpler addressing.
+#ifndef FG_ITEM_ROWS
+#define FG_ITEM_ROWS 16
+#endif
+constexpr int kIR = FG_ITEM_ROWS;  // slices per stage of the 16-column item kernel (multiple of kE)
+static_assert(kIR % kE == 0 && kIR <= 32, "item stage rows");
+
 template <int TP>
 __host__ __device__ constexpr int item_threads() { return TP / 16 * 32 + 32; }
 template <int TP>
 __host__ __device__ constexpr int item_box_chunks() { return TP == 96 ? 6 : 4; }  // 16-point chunks per TMA box
 template <int TP>
-__host__ __device__ constexpr int item_stage_bytes() { return kE * TP * (int)sizeof(double); }  // multiple of 1024 (swizzle atom)
+__host__ __device__ constexpr int item_stage_bytes() { return kIR * TP * (int)sizeof(double); }  // multiple of 1024 (swizzle atom)
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             uint64_t* bar, uint64_t pol) {
@@ -1676,33 +1591,31 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// One ring stage of an item with MTE live M tiles, B fragments at the
-// swizzled byte offsets boff[ks][j] of the stage (see fg_block_item_kernel).
-template <int MTE, int MT, int NT, int CP>
-__device__ __forceinline__ void item_stage_sw(double (&d)[MT][NT][2], const double* cs, const unsigned char* rs,
-                                              const int (&boff)[kE / 4][NT], int nr, int fk, int lane,
-                                              uint64_t* empty_s, double* sink_w) {
+// One ring stage of an item with MTE live M tiles: A fragments (coefficients)
+// at shared address ca (+ e·CP + 8i doubles), B fragments at the swizzled byte
+// offsets boff of the stage at ra.  FULL: all kE rows belong to the item (no
+// masking).  Before its DMMAs the warp releases the PREVIOUS stage's slot
+// (pend): the release depends on the last DMMA result of that stage, which was
+// only issued once every fragment it and the DMMAs before it read had arrived
+// in registers — so the producer cannot overwrite rows still being read, and
+// the release costs one dependent store instead of a warp-wide reduction of the
+// loaded values.
+template <int MTE, int MT, int NT, int CP, bool FULL>
+__device__ __forceinline__ void item_stage_sw(double (&d)[MT][NT][2], uint32_t ca, uint32_t ra,
+                                              const uint32_t (&boff)[kE / 4][NT], int nr, int fk, int lane,
+                                              uint64_t* pend, double* sink_w) {
     double af[kE / 4][MTE], bf[kE / 4][NT];
-    uint32_t xr = 0;
 #pragma unroll
     for (int ks = 0; ks < kE / 4; ++ks) {
         const int e = ks * 4 + fk;
 #pragma unroll
-        for (int i = 0; i < MTE; ++i) {
-            af[ks][i] = e < nr ? cs[e * CP + 8 * i] : 0.0;
-            const unsigned long long w = (unsigned long long)__double_as_longlong(af[ks][i]);
-            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
-        }
+        for (int i = 0; i < MTE; ++i)
+            af[ks][i] = (FULL || e < nr) ? lds_f64(ca + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            // rows past the item's end hold other slices (or unwritten ones): masked
-            bf[ks][j] = e < nr ? *reinterpret_cast<const double*>(rs + boff[ks][j]) : 0.0;
-            const unsigned long long w = (unsigned long long)__double_as_longlong(bf[ks][j]);
-            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
-        }
+        for (int j = 0; j < NT; ++j)  // rows past the item's end hold other (or unwritten) slices: masked
+            bf[ks][j] = (FULL || e < nr) ? lds_f64(ra + boff[ks][j]) : 0.0;
     }
-    xr = __reduce_xor_sync(0xffffffffu, xr);
-    if (lane == 0) mbar_arrive_after(empty_s, (double)xr, sink_w);
+    if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1] + d[0][NT - 1][1], sink_w);
 #pragma unroll
     for (int ks = 0; ks < kE / 4; ++ks)
 #pragma unroll
@@ -1722,13 +1635,13 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
     constexpr int C = item_box_chunks<TP>();
     constexpr int NB = NW / C;                       // boxes per stage
     constexpr int SB = item_stage_bytes<TP>();
-    constexpr int BOXB = C * kE * 128;               // bytes per box
+    constexpr int BOXB = C * kIR * 128;              // bytes per box
     static_assert(NB * C == NW && SB % 1024 == 0 && BOXB % 1024 == 0, "item tile / box geometry");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // swizzle-128B boxes need 1024-byte aligned destinations (1 KB of slack is allocated)
     unsigned char* rows = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // [kStages][SB]
-    double* coef = reinterpret_cast<double*>(rows + (size_t)kStages * SB);              // [kStages*kE][CP]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kE * CP);
+    double* coef = reinterpret_cast<double*>(rows + (size_t)kStages * SB);              // [kStages*kIR][CP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kIR * CP);
     uint64_t* empty = full + kStages;
     double* sink = reinterpret_cast<double*>(empty + kStages);
 
@@ -1758,9 +1671,9 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
                     const int r = (int)(it.t_first % it.stride);
                     const int j_first = (int)(it.t_first / it.stride);
                     const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
-                    for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+                    for (int64_t j0 = 0; j0 < it.n_slices; j0 += kIR, ++g) {
                         const int s = (int)(g % kStages);
-                        const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
+                        const int nr = (int)((it.n_slices - j0) < kIR ? (it.n_slices - j0) : kIR);
                         if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
                         const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
                         mbar_expect_tx(&full[s], (uint32_t)SB + cbytes);
@@ -1768,7 +1681,7 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
                         for (int b = 0; b < NB; ++b)
                             tma_load_4d(rows + (size_t)s * SB + b * BOXB, map, 0, chunk0 + b * C, r,
                                         j_first + (int)j0, &full[s], pol);
-                        bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, cbytes, &full[s]);
+                        bulk_g2s(coef + (size_t)s * kIR * CP, c0 + j0 * CP, cbytes, &full[s]);
                     }
                 }
             }  // tiles
@@ -1780,15 +1693,16 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
     // byte offsets of this lane's B fragments in a stage: slice e = 4ks + fk,
     // point 16·warp + 8j + fr → box warp / C, line L = e·C + warp % C, 16-byte
     // unit (4j + fr/2) XOR (L mod 8), half (fr & 1)
-    int boff[kE / 4][NT];
+    uint32_t boff[kE / 4][NT];
 #pragma unroll
     for (int ks = 0; ks < kE / 4; ++ks)
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
             const int L = (ks * 4 + fk) * C + warp % C;
             const int u = (4 * j + (fr >> 1)) ^ (L & 7);
-            boff[ks][j] = (warp / C) * BOXB + L * 128 + u * 16 + (fr & 1) * 8;
+            boff[ks][j] = (uint32_t)((warp / C) * BOXB + L * 128 + u * 16 + (fr & 1) * 8);
         }
+    const uint32_t rows_s = smem_u32(rows), coef_s = smem_u32(coef) + (uint32_t)(fr * 8);
     double d[MT][NT][2];
     int64_t g = 0;
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
@@ -1812,19 +1726,39 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
         for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
-        for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
+        uint64_t* pend = nullptr;  // slot of the previous stage, released by the next one
+        for (int64_t j0 = 0; j0 < it.n_slices; j0 += kIR, ++g) {
             const int s = (int)(g % kStages);
             mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
-            const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
-            const unsigned char* rs = rows + (size_t)s * SB;
-            const double* cs = coef + (size_t)s * kE * CP + fr;
-            // warp-uniform branch per item: only the item's M tiles are issued
-            // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
-            if (mt > 1)
-                item_stage_sw<2, MT, NT, CP>(d, cs, rs, boff, nr, fk, lane, &empty[s], sink + warp);
-            else
-                item_stage_sw<1, MT, NT, CP>(d, cs, rs, boff, nr, fk, lane, &empty[s], sink + warp);
+            const int nr = (int)((it.n_slices - j0) < kIR ? (it.n_slices - j0) : kIR);
+            // a stage's kIR rows in groups of kE (fragment registers for kE rows
+            // only); the previous stage's slot is released after the first group's loads
+#pragma unroll
+            for (int h = 0; h < kIR / kE; ++h) {
+                const int nrh = nr - h * kE;  // rows of this group that belong to the item
+                if (nrh <= 0) break;          // warp-uniform
+                const uint32_t ra = rows_s + (uint32_t)(s * SB + h * kE * C * 128);
+                const uint32_t ca = coef_s + (uint32_t)((s * kIR + h * kE) * CP * 8);
+                uint64_t* rel = h == 0 ? pend : nullptr;
+                // warp-uniform branches per item and group: only the item's M tiles
+                // are issued (predicated-off DMMAs would still occupy the fp64 tensor
+                // pipe), and only a partial last group masks its rows
+                if (nrh >= kE) {
+                    if (mt > 1)
+                        item_stage_sw<2, MT, NT, CP, true>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
+                    else
+                        item_stage_sw<1, MT, NT, CP, true>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
+                } else {
+                    if (mt > 1)
+                        item_stage_sw<2, MT, NT, CP, false>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
+                    else
+                        item_stage_sw<1, MT, NT, CP, false>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
+                }
+            }
+            pend = &empty[s];
         }
+        // the item's last stage: released once its DMMAs are done (the flush needs them anyway)
+        if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1] + d[0][NT - 1][1], sink + warp);
         const uint64_t keep = l2_policy_last();  // the steps read P next
         // flush into P (this CTA owns the tile, items in table order, so the
         // sum of each step is deterministic): the first item of a step stores,
@@ -1856,7 +1790,7 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
 
 template <int TP, int NS>
 size_t item_block_smem() {
-    return 1024 + (size_t)NS * item_stage_bytes<TP>() + (size_t)NS * kE * kItemPitch * sizeof(double) +
+    return 1024 + (size_t)NS * item_stage_bytes<TP>() + (size_t)NS * kIR * kItemPitch * sizeof(double) +
            (2 * NS) * sizeof(uint64_t) + (TP / 16) * sizeof(double);
 }
 
@@ -2169,10 +2103,10 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
 // ---- fused step pairs (fg_step2_kernel) -------------------------------------
 // Eligible plans: blocked 1D/2D fields whose halo (one row) is at most
 // kPairMaxHalo points, one warp column per tile (split 1), adaptive or full
-// memory, m = 0 from the stencil.  FGB200_PAIRS=0 disables.
-bool pairs_enabled(const fg_plan* p) {
-    const char* e = getenv("FGB200_PAIRS");  // read per call (tests toggle it)
-    if (e && e[0] == '0') return false;
+// memory, m = 0 from the stencil, with the caller's pair scratch (pair_dev).
+// FG_RUN_NO_PAIRS disables them, FG_RUN_PAIRS enables them in 2D.
+bool pairs_enabled(const fg_plan* p, int32_t flags) {
+    if ((flags & FG_RUN_NO_PAIRS) || !p->pair_dev) return false;
     if (!p->tblock || p->tblock % 2 || p->ndim > 2 || p->kind == FG_MEM_SHORT || p->subblock) return false;
     if (p->step_flags & FG_STEP_M0_FROM_HISTORY) return false;
     if (choose_split(p) != 1 || tile_points(1) != kPairTile) return false;
@@ -2180,39 +2114,8 @@ bool pairs_enabled(const fg_plan* p) {
     // halo = one 256-point row) 33.4 -> 32.9 ms only — a pair CTA recomputes a
     // halo as large as its tile and needs ~95 registers, so one pair CTA per SM
     // fits beside the block stage and consecutive pairs barely overlap
-    if (!(e && e[0] == '1') && p->ndim != 1) return false;
+    if (!(flags & FG_RUN_PAIRS) && p->ndim != 1) return false;
     return (p->ndim == 1 ? 1 : p->shape[1]) <= kPairMaxHalo;
-}
-
-// Library scratch of pair launches: the alternate field buffer and *u3_step.
-struct PairScratch {
-    int dev = -1;
-    double* u3 = nullptr;
-    int64_t n = 0;
-    int64_t* step = nullptr;
-    ~PairScratch() {
-        if (u3) cudaFree(u3);
-        if (step) cudaFree(step);
-    }
-};
-
-int pair_scratch(const fg_plan* p, PairScratch** out) {
-    static thread_local PairScratch ps;
-    int cur = 0;
-    if (int rc = cuda_check(cudaGetDevice(&cur), "cudaGetDevice")) return rc;
-    const int64_t n = p->B * p->ms;
-    if (ps.dev != cur || ps.n < n) {
-        if (ps.u3) cudaFree(ps.u3);
-        if (ps.step) cudaFree(ps.step);
-        ps.u3 = nullptr;
-        ps.step = nullptr;
-        if (int rc = cuda_check(cudaMalloc(&ps.u3, (size_t)n * sizeof(double)), "pair field buffer")) return rc;
-        if (int rc = cuda_check(cudaMalloc(&ps.step, sizeof(int64_t)), "pair step")) return rc;
-        ps.n = n;
-        ps.dev = cur;
-    }
-    *out = &ps;
-    return FG_OK;
 }
 
 constexpr size_t kPairSmem = (size_t)(kPairTile + 4 * kPairMaxHalo + kPairTile + 2 * kPairMaxHalo) * sizeof(double);
@@ -2302,11 +2205,10 @@ BlockVariant block_variant_of(bool staged, bool tail, int tp) {
 
 // tail: the variant with the small ring (see kTailStages)
 BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
-    static const char* force = getenv("FGB200_BLOCK_TP");
     const int cands[4] = {256, 224, 192, 128};
     const bool staged = p->B == 1 && p->blkcoef_dev;
     BlockVariant best = {nullptr, 0, 0};
-    auto usable = [&](int tp) { return force ? atoi(force) == tp : !(p->tblock == 32 && tp == 256); };  // 32 x 256 spills
+    auto usable = [&](int tp) { return !(p->tblock == 32 && tp == 256); };  // 32 x 256 spills
     auto cost_of = [&](int tp) {
         const int64_t tiles = ((p->n_m + tp - 1) / tp) * p->B;
         return ((tiles + sm_count() - 1) / sm_count()) * tp;
@@ -2333,14 +2235,11 @@ BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
     return best;
 }
 
-// Block-kernel grid: ensembles one CTA per tile; single members at most
-// FGB200_BLOCK_CTAS_PER_SM (default 2) CTAs per SM looping over tiles (one wave;
-// 1 leaves room for the concurrent steps but halves the stream rate).
+// Block-kernel grid: ensembles one CTA per tile; single members two CTAs per SM
+// looping over tiles (one wave; two step CTAs still fit beside them per SM).
 unsigned block_grid(const fg_plan* p, int64_t total_tiles) {
     if (p->B != 1) return (unsigned)total_tiles;
-    const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
-    const int per = e ? atoi(e) : 2;
-    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
+    const int64_t cap = (int64_t)sm_count() * 2;
     return (unsigned)(total_tiles < cap ? total_tiles : cap);
 }
 
@@ -2373,8 +2272,6 @@ BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& 
 // FGB200_ITEM_COLS, else 16 for ensembles and 8 for a single member.
 int item_cols(const fg_plan* p) {
     if (p->item_cols == 8 || p->item_cols == 16) return p->item_cols;
-    static const char* e = getenv("FGB200_ITEM_COLS");
-    if (e && (atoi(e) == 8 || atoi(e) == 16)) return atoi(e);
     return p->B > 1 ? 16 : 8;
 }
 
@@ -2540,18 +2437,16 @@ int launch_item_coef(const BlockArgs& a, const ItemTable& T, cudaStream_t st) {
 // Item partial sums (coefficient rows already built) into Q, then the ordered
 // reduction into P (or directly into P for a single all-steps item).
 #ifndef FG_ITEM_STAGES
-#define FG_ITEM_STAGES 8
+#define FG_ITEM_STAGES (64 / FG_ITEM_ROWS)
 #endif
-constexpr int kItemMainStages = FG_ITEM_STAGES;  // two main CTAs per SM: 2 x 70 KB of ring at TP 112
-constexpr int kItemTailStages = 3;  // tail launches run beside the main CTAs
+constexpr int kItemMainStages = FG_ITEM_STAGES;  // two main CTAs per SM: 64 slice rows of ring each
+constexpr int kItemTailStages = 24 / kIR > 2 ? 24 / kIR : 2;  // tail launches run beside the main CTAs
 
 // Item-kernel tile width: two CTAs per SM (two independent rings, so one
 // CTA's flushes overlap the other's stream), so pick the TP (16-point warps)
 // that minimises the busiest CTA's points, ceil(tiles / (2 SMs)) * TP (c2: 586
 // tiles of 112 = 2 per CTA; ensembles of 512-point members: 128, no partial tiles).
 int choose_item_tp(const fg_plan* p) {
-    static const char* force = getenv("FGB200_ITEM_TP");
-    if (force) return atoi(force);
     const int cands[2] = {128, 96};  // the 16-column kernel's swizzled box geometries
     int best = 128;
     int64_t best_cost = INT64_MAX;
@@ -2588,9 +2483,7 @@ int launch_item8_sums(const fg_plan* p, const BlockArgs& a, const ItemTable& T, 
                             "item smem attribute"))
         return rc;
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
-    const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
-    const int per = e ? atoi(e) : 2;
-    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
+    const int64_t cap = (int64_t)sm_count() * 2;
     ++g_launches;
     kern<<<(unsigned)(a.total_tiles < cap ? a.total_tiles : cap), tp + 32, smem, st>>>(a, T);
     return cuda_check(cudaGetLastError(), "fg_block_item8 launch");
@@ -2627,7 +2520,7 @@ int encode_item_maps(const fg_plan* p, ItemTable& T, int tp, ItemMaps& M) {
     for (int x = 0; x < T.n_items; ++x) {
         BlockItem& it = T.it[x];
         const int64_t s = it.stride;
-        const int64_t j_end = it.t_first / s + ((int64_t)(it.n_slices + kE - 1) / kE) * kE;  // boxes end (exclusive)
+        const int64_t j_end = it.t_first / s + ((int64_t)(it.n_slices + kIR - 1) / kIR) * kIR;  // boxes end (exclusive)
         if (j_end > halloc / s)
             return fail(FG_ERR_ARG,
                         "history allocation of %lld slices is too small for the item stream: stride %lld reads "
@@ -2641,7 +2534,7 @@ int encode_item_maps(const fg_plan* p, ItemTable& T, int tp, ItemMaps& M) {
             const cuuint64_t dims[4] = {16, (cuuint64_t)(p->B * p->ms / 16), (cuuint64_t)s, (cuuint64_t)(halloc / s)};
             const cuuint64_t gstride[3] = {128, slice_bytes, (cuuint64_t)s * slice_bytes};
             const cuuint32_t box[4] = {16, (cuuint32_t)(tp == 96 ? item_box_chunks<96>() : item_box_chunks<128>()),
-                                       1, (cuuint32_t)kE};
+                                       1, (cuuint32_t)kIR};
             const cuuint32_t estride[4] = {1, 1, 1, 1};
             const CUresult r = enc(&M.map[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, box,
                                    estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -2681,9 +2574,7 @@ int launch_item_sums(const fg_plan* p, const BlockArgs& a, ItemTable& T, int tp,
     if (int rc = prefer_max_smem((const void*)kern)) return rc;
     // two CTAs per SM (FGB200_BLOCK_CTAS_PER_SM) loop over tiles and walk all
     // items per tile: a CTA owns its tile's P rows, so the items' adds need no atomics
-    const char* e = getenv("FGB200_BLOCK_CTAS_PER_SM");
-    const int per = e ? atoi(e) : 2;
-    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
+    const int64_t cap = (int64_t)sm_count() * 2;
     ItemMaps M;
     if (int rc = encode_item_maps(p, T, tp, M)) return rc;
     ++g_launches;
@@ -2712,11 +2603,6 @@ int launch_dense_coef(const fg_plan* p, const BlockArgs& a, cudaStream_t st) {
     return cuda_check(cudaGetLastError(), "fg_block_coef launch");
 }
 
-// FGB200_BLOCK_ITEMS=0 forces the dense main launch (same results within rounding).
-bool items_enabled() {
-    const char* e = getenv("FGB200_BLOCK_ITEMS");
-    return !(e && e[0] == '0');
-}
 
 // Tail launches of factors above kMaxDenseTBlock are itemized too (the dense
 // kernel's accumulators would not fit).
@@ -2724,7 +2610,7 @@ bool items_enabled() {
 // tail does not fit the item table they fall back to the dense kernel, which
 // builds per-member coefficient tables in the CTA.
 bool item_tail(const fg_plan* p) {
-    return p->tblock > kMaxDenseTBlock || (p->B > 1 && p->blkcoef_dev && items_enabled());
+    return p->tblock > kMaxDenseTBlock || (p->B > 1 && p->blkcoef_dev);
 }
 
 int64_t tail_begin(const fg_plan* p, int64_t kb0) { return kb0 - p->tblock > 0 ? kb0 - p->tblock : 0; }
@@ -2775,8 +2661,7 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
             row0 = (p->tblock * cp + ip - 1) / ip;  // dense tail rows, in item-pitch rows
         }
         ItemTable T;
-        const bool ok = items_enabled() || p->tblock > kMaxDenseTBlock;
-        if (ok && build_items(p, kb0, bt, 0, a.t_end, T, row0)) {
+        if (build_items(p, kb0, bt, 0, a.t_end, T, row0)) {
             if (T.n_items == 0)
                 return cuda_check(
                     cudaMemsetAsync(block_P(p, kb0), 0, (size_t)p->tblock * p->B * p->ms * sizeof(double), st),
@@ -2940,11 +2825,6 @@ struct BlockTrace {
     }
 };
 
-// FGB200_BLOCK_OVERLAP=0 turns the side-stream pipeline off (same results).
-bool overlap_enabled() {
-    const char* e = getenv("FGB200_BLOCK_OVERLAP");
-    return !(e && e[0] == '0');
-}
 
 // Per-thread side stream (lowest priority, so the latency-bound steps win SM
 // slots as they free) and its fork/join events, on the current device.
@@ -3053,8 +2933,8 @@ int launch_persistent(const fg_plan* p, int64_t k0, int64_t k1, double* pool, cu
 }
 
 // Key of a cached run graph (fg_run_ex with FG_RUN_GRAPH): the plan bytes (every
-// device pointer and scalar), the step range, the snapshot list and targets,
-// the flags and the environment knobs that shape the launches.
+// device pointer and scalar, incl. the caller's scratch buffers), the step
+// range, the snapshot list and targets, and the flags.
 struct GraphKey {
     fg_plan plan;
     int64_t k0 = -1, k1 = -1;
@@ -3062,12 +2942,11 @@ struct GraphKey {
     const double* host_pool = nullptr;
     int32_t flags = 0;
     std::vector<int64_t> snaps;
-    std::string env;
     std::vector<double> psi_host;  // host coefficients baked into the step launches
     GraphKey() { memset(&plan, 0, sizeof plan); }
     bool operator==(const GraphKey& o) const {
         return memcmp(&plan, &o.plan, sizeof plan) == 0 && k0 == o.k0 && k1 == o.k1 && pool == o.pool &&
-               host_pool == o.host_pool && flags == o.flags && snaps == o.snaps && env == o.env &&
+               host_pool == o.host_pool && flags == o.flags && snaps == o.snaps &&
                psi_host.size() == o.psi_host.size() &&
                (psi_host.empty() || memcmp(psi_host.data(), o.psi_host.data(), psi_host.size() * sizeof(double)) == 0);
     }
@@ -3084,112 +2963,7 @@ struct GraphCache {
     ~GraphCache() { reset(); }
 };
 
-std::string graph_env() {
-    std::string e;
-    for (const char* v : {"FGB200_BLOCK_OVERLAP", "FGB200_BLOCK_ITEMS", "FGB200_BLOCK_TP", "FGB200_BLOCK_CTAS_PER_SM"}) {
-        const char* x = getenv(v);
-        e += x ? x : "-";
-        e += '|';
-    }
-    return e;
-}
 
-// Library scratch of chain launches (per thread, grown on demand; not in the
-// plan so the ABI is unchanged): tile flags and the block's recent table.
-struct ChainScratch {
-    int dev = -1;
-    unsigned long long* flags = nullptr;
-    int64_t n_flags = 0;
-    RecentRow* tab = nullptr;
-    ~ChainScratch() {
-        if (flags) cudaFree(flags);
-        if (tab) cudaFree(tab);
-    }
-};
-
-int chain_scratch(int64_t tiles, ChainScratch** out) {
-    static thread_local ChainScratch cs;
-    int cur = 0;
-    if (int rc = cuda_check(cudaGetDevice(&cur), "cudaGetDevice")) return rc;
-    if (cs.dev != cur || cs.n_flags < tiles) {
-        if (cs.flags) cudaFree(cs.flags);
-        if (cs.tab) cudaFree(cs.tab);
-        cs.flags = nullptr;
-        cs.tab = nullptr;
-        if (int rc = cuda_check(cudaMalloc(&cs.flags, (size_t)tiles * sizeof(unsigned long long)), "chain flags"))
-            return rc;
-        if (int rc = cuda_check(cudaMalloc(&cs.tab, (size_t)kMaxTBlock * sizeof(RecentRow)), "chain table")) return rc;
-        cs.n_flags = tiles;
-        cs.dev = cur;
-    }
-    *out = &cs;
-    return FG_OK;
-}
-
-// Chain launches need every tile's CTA resident at once on an otherwise idle
-// GPU (one tile per CTA), so a tile never waits on a CTA that cannot start;
-// the concurrent block-stage CTAs never wait on the steps, so at worst they
-// delay, never block, the chain's CTAs.
-bool chain_fits(const fg_plan* p) {
-    if (!p->tblock || choose_split(p) != 1) return false;
-    const int64_t tiles = tiles_of(p, 1);
-    int per_sm = 0;
-    StepKernel kern = pick_kernel(p->ndim, p->reaction, 1, true);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, acc_smem(1, 1)) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return per_sm > 0 && tiles <= (int64_t)per_sm * sm_count();
-}
-
-// Stencil reach in tiles of one member: the farthest neighbour offset (1D 1,
-// 2D n1, 3D n1*n2 points) rounded up to whole tiles.
-int chain_dep(const fg_plan* p) {
-    const int64_t reach = p->ndim == 1 ? 1 : p->ndim == 2 ? p->shape[1] : p->shape[1] * p->shape[2];
-    const int64_t tp = tile_points(1);
-    return (int)((reach + tp - 1) / tp);
-}
-
-// Steps [k0, k1) of the temporal block kb0 in one chain launch; snapshots
-// (at most kChainSnaps) of steps in (k0, k1] go to pool slots snap_slot[i].
-int launch_chain(const fg_plan* p, int64_t k0, int64_t k1, int64_t kb0, double* pool, const int64_t* snap_step,
-                 const int32_t* snap_slot, int n_snap, cudaStream_t st) {
-    StepArgs a = make_args(p, 1);
-    ChainScratch* cs = nullptr;
-    if (int rc = chain_scratch(a.total_tiles, &cs)) return rc;
-    if (n_snap > kChainSnaps) return fail(FG_ERR_ARG, "chain launch: too many snapshots");
-    a.k0 = k0;
-    a.k1 = k1;
-    a.pool = pool;
-    a.n_csnap = n_snap;
-    for (int i = 0; i < n_snap; ++i) {
-        a.csnap_step[i] = snap_step[i];
-        a.csnap_slot[i] = snap_slot[i];
-    }
-    a.passes = 1;
-    a.blocked = 1;
-    a.kb0 = kb0;
-    a.P = block_P(p, kb0);
-    a.chain = 1;
-    a.dep = chain_dep(p);
-    a.flags = cs->flags;
-    a.rtab = cs->tab;
-    a.has_rc = p->B == 1 ? 1 : 0;
-    const int bt = (int)(k1 - kb0);
-    ++g_launches;
-    fg_recent_table_kernel<<<1, 128, 0, st>>>(cs->tab, p->kind, kb0, bt, p->base, a.hz_max, p->psi_dev, a.has_rc);
-    if (int rc = cuda_check(cudaGetLastError(), "fg_recent_table launch")) return rc;
-    if (int rc = cuda_check(cudaMemsetAsync(cs->flags, 0, (size_t)a.total_tiles * sizeof(unsigned long long), st),
-                            "chain flags reset"))
-        return rc;
-    if (int rc = cuda_check(cudaMemsetAsync(p->status_dev + 1, 0, sizeof(int64_t), st), "chain counter reset"))
-        return rc;
-    StepKernel kern = pick_kernel(p->ndim, p->reaction, 1, true);
-    if (int rc = prefer_max_smem((const void*)kern)) return rc;
-    ++g_launches;
-    kern<<<(unsigned)a.total_tiles, kThreads, acc_smem(1, 1), st>>>(a);
-    return cuda_check(cudaGetLastError(), "fg_step chain launch");
-}
 
 }  // namespace
 
@@ -3330,20 +3104,12 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         persistent = G > 0 && snaps_ok;  // else fall back to per-step launches
     }
     double* ppool = n_snap > 0 ? pool : nullptr;
-    // chain launches (one per temporal block, tiles synchronised pairwise)
-    const bool chain = (flags & FG_RUN_CHAIN) && !persistent && tb && chain_fits(p) && p->subblock == 0;
     // sub-block launches (per-step launch modes only)
-    const bool sub = tb && p->subblock > 0 && !persistent && !chain;
-    // fused step pairs (per-step launch modes, small 1D/2D fields)
-    const bool pairs = tb && !persistent && !chain && !sub && pairs_enabled(p);
-    PairScratch* ps = nullptr;
-    if (pairs) {  // allocated here, never inside a graph capture
-        if (int rc = pair_scratch(p, &ps)) return rc;
-    }
-    if (chain) {
-        ChainScratch* cs = nullptr;  // allocated here, never inside a graph capture
-        if (int rc = chain_scratch(tiles_of(p, 1), &cs)) return rc;
-    }
+    const bool sub = tb && p->subblock > 0 && !persistent;
+    // fused step pairs (per-step launch modes, small 1D/2D fields, caller scratch)
+    const bool pairs = tb && !persistent && !sub && pairs_enabled(p, flags);
+    double* const u3 = pairs ? p->pair_dev : nullptr;                                      // u^{k+2} buffer
+    int64_t* const u3_step = pairs ? reinterpret_cast<int64_t*>(p->pair_dev + p->B * p->ms) : nullptr;
 
     const int pdl = (flags & FG_RUN_PDL) ? 1 : 0;
     const bool graph = (flags & FG_RUN_GRAPH) != 0 && !persistent;
@@ -3361,7 +3127,6 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         key.host_pool = host_pool;
         key.flags = flags;
         key.snaps.assign(snap_steps, snap_steps + (n_snap > 0 ? n_snap : 0));
-        key.env = graph_env();
         if (p->psi_host && p->tblock) key.psi_host.assign(p->psi_host, p->psi_host + p->tblock + 1);
         if (gc.exec && gc.key == key) {
             g_launches += gc.kernels;
@@ -3428,24 +3193,6 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         return (int)FG_OK;
     };
     // persistent launch over [ka, kz): its snapshots are copied after it
-    // chain launch over [ka, kz) (inside one block); blocks with more snapshots
-    // than a launch carries, or a single step, use per-step launches
-    auto chain_steps = [&](int64_t ka, int64_t kz, int64_t kb0, bool first_after_block) {
-        int64_t sst[kChainSnaps];
-        int32_t ssl[kChainSnaps];
-        int ns = 0;
-        int64_t j = si;
-        for (; j < n_snap && snap_steps[j] <= kz; ++j) {
-            if (ns == kChainSnaps) return steps(ka, kz, kb0, first_after_block);
-            sst[ns] = snap_steps[j];
-            ssl[ns++] = (int32_t)j;
-        }
-        if (kz - ka < 2) return steps(ka, kz, kb0, first_after_block);
-        const int64_t i0 = si;
-        if (int r = launch_chain(p, ka, kz, kb0, pool, sst, ssl, ns, cap)) return r;
-        si = j;
-        return copy_out(i0, si);
-    };
     // the steps [ka, kz) of block kb0 as fused pairs (an even number of them, so
     // the field is back in its parity buffer), then single steps for the rest
     auto pair_steps = [&](int64_t ka, int64_t kz, int64_t kb0, bool first) -> int {
@@ -3460,10 +3207,10 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
             if (si < n_snap && snap_steps[si] == k + 2) snap2 = pool + (si++) * slice;
             const bool wait = pdl && k > k0 && !(k == ka && first);
             const bool even = (i % 2) == 0;
-            const double* uin = even ? p->u_dev[k & 1] : ps->u3;
-            double* uout = even ? ps->u3 : p->u_dev[k & 1];
+            const double* uin = even ? p->u_dev[k & 1] : u3;
+            double* uout = even ? u3 : p->u_dev[k & 1];
             if (int r = launch_pair(p, k, kb0, snap1, snap2, cap, wait, pdl, uin, p->u_dev[(k + 1) & 1], uout,
-                                    even ? 1 : 0, ps->step))
+                                    even ? 1 : 0, u3_step))
                 return r;
             if (si > i0)
                 if (int r = copy_out(i0, si)) return r;
@@ -3537,10 +3284,10 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         };
         cudaStream_t side = nullptr;
         cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
-        if (overlap_enabled()) rc = side_stream(&side, &ev_fork, ev_join);
+        if (!(flags & FG_RUN_NO_OVERLAP)) rc = side_stream(&side, &ev_fork, ev_join);
         if (rc == FG_OK && sub) rc = sub_stream(&sstream, &sready, sdone);
         if (rc == FG_OK && pairs)
-            rc = cuda_check(cudaMemsetAsync(ps->step, 0xff, sizeof(int64_t), cap), "pair step reset");  // -1
+            rc = cuda_check(cudaMemsetAsync(u3_step, 0xff, sizeof(int64_t), cap), "pair step reset");  // -1
         int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
         BlockTrace tr(graph ? nullptr : getenv("FGB200_TRACE"));
         for (int64_t kb = k0 - k0 % tb; kb < k1 && rc == FG_OK; kb += tb) {
@@ -3572,7 +3319,6 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
                 if (rc != FG_OK) break;
             }
             rc = persistent ? persistent_steps(ks, ke, kb)
-                 : chain    ? chain_steps(ks, ke, kb, start)
                  : sub      ? sub_steps(ks, ke, kb, block_len(kb), start)
                  : pairs    ? pair_steps(ks, ke, kb, start)
                             : steps(ks, ke, kb, start);
@@ -3581,7 +3327,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
             const int64_t nf = p->B * p->ms;
             ++g_launches;
             fg_u3_fixup_kernel<<<(unsigned)((nf + 255) / 256 < 1024 ? (nf + 255) / 256 : 1024), 256, 0, cap>>>(
-                p->status_dev, ps->step, ps->u3, p->u_dev[0], p->u_dev[1], nf);
+                p->status_dev, u3_step, u3, p->u_dev[0], p->u_dev[1], nf);
             rc = cuda_check(cudaGetLastError(), "fg_u3_fixup launch");
         }
         if (main_on_side >= 0) {  // error path: never leave the side stream unjoined
@@ -3723,7 +3469,7 @@ int fg_history_pad(int32_t kind, int64_t n_steps, int64_t base, int64_t* pad) {
             a_prev *= base;
         }
     }
-    *pad = (kE - 1) * s_max;
+    *pad = (kIR - 1) * s_max;
     return FG_OK;
 }
 

@@ -560,8 +560,8 @@ def test_temporal_blocking_modes_bitwise(fg, golden, name, monkeypatch):
     cfg = _any_field_config(fg, golden, name)
     ref = fg.run_field(cfg, flags=0, tblock=16)
     for kw in (dict(flags=1), dict(flags=2), dict(flags=3), dict(flags=4), dict(progress_every=7),
-               dict(progress_every=16), dict(flags=2, overlap="0"), dict(flags=1, overlap="0"), dict(flags=34),
-               dict(flags=32), dict(flags=35), dict(flags=34, progress_every=7), dict(flags=34, overlap="0")):
+               dict(progress_every=16), dict(flags=2, overlap="0"), dict(flags=1, overlap="0"),
+               dict(flags=3, overlap="0"), dict(flags=2, progress_every=7)):
         kw = dict(kw)
         monkeypatch.setenv("FGB200_BLOCK_OVERLAP", kw.pop("overlap", "1"))
         got = fg.run_field(cfg, tblock=16, **kw)
@@ -570,7 +570,7 @@ def test_temporal_blocking_modes_bitwise(fg, golden, name, monkeypatch):
             assert s0 == s1 and np.array_equal(a0, a1), kw
 
 
-@pytest.mark.parametrize("flags", [2, 34])
+@pytest.mark.parametrize("flags", [1, 2, 4])
 def test_temporal_blocking_divergence(fg, golden, flags):
     u0 = np.zeros((8, 8))
     u0[4, 4] = 10.0
@@ -580,25 +580,25 @@ def test_temporal_blocking_divergence(fg, golden, flags):
     assert exc.value.step == golden.meta["divergence"]["step"]
 
 
-@pytest.mark.parametrize("shape", [(256, 256), (96, 200), (4000,), (20, 24, 40)])
-def test_chain_launches_bitwise(fg, shape):
-    """Chain launches (one per block, tiles synchronised with their stencil
-    neighbours) equal per-step launches bitwise, incl. odd row strides, several
-    tiles per row and 3D planes spanning many tiles; divergence reports the
-    same step and peak."""
-    rng = np.random.default_rng(11)
-    u0 = rng.uniform(0.0, 1.0, size=shape)
-    for ax in range(len(shape)):
-        idx = [slice(None)] * len(shape)
-        idx[ax] = 0
-        u0[tuple(idx)] = 0.0
-        idx[ax] = -1
-        u0[tuple(idx)] = 0.0
-    dx = 1.0 / (shape[-1] - 1)
-    dt = (0.05 * dx**2) ** (1 / 0.7)
-    cfg = fg.FieldConfig(initial=u0, dx=dx, gamma=0.7, dt=dt, n_steps=300, strategy=fg.AdaptiveMemory(4),
-                         snapshot_every=23, history_byte_cap=None)
-    ref = fg.run_field(cfg, flags=2, tblock=64)
-    got = fg.run_field(cfg, flags=34, tblock=64)
-    for (s0, a0), (s1, a1) in zip(ref.snapshots, got.snapshots):
-        assert s0 == s1 and np.array_equal(a0, a1), s0
+def test_graph_replay_after_a_larger_plan(fg, monkeypatch):
+    """A cached run graph replays its own plan's buffers: graph run A, a run of
+    a larger 1D field (fused pairs, their scratch owned by that plan), then
+    graph run A again gives A's results bitwise (the pair scratch is part of
+    the plan, so a graph never captures another run's buffers)."""
+    monkeypatch.setenv("FGB200_PAIRS", "1")
+
+    def cfg_of(n):
+        x = np.linspace(0.0, 1.0, n)
+        u0 = np.exp(-((x - 0.4) ** 2) / 0.01)
+        u0[0] = u0[-1] = 0.0
+        return fg.FieldConfig(initial=u0, dx=x[1], gamma=0.6, dt=(0.2 * x[1] ** 2) ** (1 / 0.6), n_steps=300,
+                              strategy=fg.AdaptiveMemory(4), snapshot_every=50, history_byte_cap=None)
+
+    a, big = cfg_of(700), cfg_of(5000)
+    ref = fg.run_field(a, flags=2, tblock=32)
+    first = fg.run_field(a, flags=1, tblock=32)
+    fg.run_field(big, flags=1, tblock=32)
+    again = fg.run_field(a, flags=1, tblock=32)
+    for res in (first, again):
+        for (s0, a0), (s1, a1) in zip(ref.snapshots, res.snapshots):
+            assert s0 == s1 and np.array_equal(a0, a1), s0
