@@ -206,13 +206,14 @@ def default_subblock(p: "Problem", tblock: int) -> int:
 
 def history_pad(p: "Problem", tblock: int) -> int:
     """Slices allocated past H[n] for a blocked run (fg_history_pad): the 16-column
-    item stage reads whole TMA boxes of 8 slices of a strided progression."""
+    item stage reads whole TMA boxes of 16 slices of a strided progression (the
+    itemized stages of adaptive runs, and the sub-block launches of dense ones)."""
     n = int(p.n_steps)
-    if not tblock or n <= tblock or p.kind != "adaptive" or item_cols(p) != 16:
+    if not tblock or n <= tblock or item_cols(p) != 16:
         return 0
     pad = C.c_int64(0)
-    _lib.check(_lib.load().fg_history_pad(_lib.MEM_KINDS["adaptive"], n, int(p.param), C.byref(pad)),
-               "fg_history_pad")
+    base = int(p.param) if p.kind == "adaptive" else 0
+    _lib.check(_lib.load().fg_history_pad(_lib.MEM_KINDS[p.kind], n, base, C.byref(pad)), "fg_history_pad")
     return int(pad.value)
 
 

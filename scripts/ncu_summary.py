@@ -37,6 +37,9 @@ KEYS = [
     "launch__grid_size",
     "lts__t_sector_hit_rate.pct",
     "smsp__average_warp_latency_issue_stalled_long_scoreboard",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
