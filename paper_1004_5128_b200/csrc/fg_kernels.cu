@@ -60,8 +60,30 @@ int cuda_check(cudaError_t e, const char* what) {
     return fail(FG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// Device-side bounds checks (FG_CHECKS builds only; compute-sanitizer is closed
+// on the GPU pool): every global index a kernel derives from its launch
+// arguments — history slice, partial-sum row, coefficient row, tensor-map
+// coordinate, step column, ψ index — is checked against the buffer it
+// addresses, and a violation traps with file/line (scripts/checked_suite.sh runs
+// the GPU tests against that build).
+#ifdef FG_CHECKS
+#define FG_DCHECK(cond)                                                                                   \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("FG_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x,  \
+                   (int)threadIdx.x, #cond);                                                              \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define FG_DCHECK(cond) ((void)0)
+#endif
+
 constexpr int kThreads = 256;   // 8 warps
-constexpr int kMinBlocks = 4;   // resident CTAs per SM the register budget targets
+#ifndef FG_STEP_MINB
+#define FG_STEP_MINB 4
+#endif
+constexpr int kMinBlocks = FG_STEP_MINB;   // resident CTAs per SM the register budget targets
 constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit load)
 constexpr int kUnroll = 8;      // slices in flight per thread
 constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
@@ -300,6 +322,8 @@ struct StepArgs {
     int32_t blocked;       // temporal blocking: slices t < kb0 come from P
     int64_t kb0;           // first step of the current block
     const double* P;       // [tblock][B*ms] block partial sums (fg_block_kernel)
+    int64_t h_slices;      // history capacity (bounds checks)
+    int32_t tblock;        // rows of P (bounds checks)
     // blocked single-step launches: the entries of step k's schedule with
     // 2 <= m <= k-kb0 (the only ones a blocked step still sums itself), host-
     // evaluated so the step kernel builds no schedule: offsets ascending, weights,
@@ -411,6 +435,7 @@ __device__ __forceinline__ void general_a_phase(const StepArgs& a, int64_t k, do
             int si = 0;
             while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
             const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
+            FG_DCHECK(m >= 2 && m <= k && k < a.h_slices);
             s_t[e] = (int32_t)(k - m);
             s_w[e] = (int32_t)segs[si].stride;
         }
@@ -536,11 +561,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 // all before the dependency wait (same order as the unblocked path)
                 const double2 pb = q < a.n_m ? ld_cg2_hint(a.P + bb * a.slice_stride + b * a.ms + q, l2_policy_first())
                                              : make_double2(0.0, 0.0);  // its only read
+                FG_DCHECK(bb >= 0 && bb < a.tblock && k < a.h_slices && rn <= bb);
                 if (q < a.n_m && rn > 0) {
                     const double* hbase = a.H + b * a.ms + q + k * a.slice_stride;
                     const double* psi_b = a.psi + b * a.psi_stride;
                     const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
-                    constexpr int kR = REACT ? 4 : 5;  // recent slices in flight per round (no spills)
+#ifndef FG_STEP_KR
+#define FG_STEP_KR 5
+#endif
+                    constexpr int kR = REACT ? FG_STEP_KR - 1 : FG_STEP_KR;  // recent slices in flight per round (no spills)
 #pragma unroll 1
                     // entries oldest first (descending m): the fused pair kernel must
                     // add the newest ones after its dependency wait, in the same order
@@ -552,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                             const int e = rn - 1 - (e0 + u);
                             const int m = e >= 0 ? rm[e] : 0;
                             const bool on = e >= 0 && m <= mmax;
+                            FG_DCHECK(!on || (m >= 2 && m <= k));
                             if (on) {
                                 v[u] = ld_stream(hbase - (int64_t)m * a.slice_stride);
                                 c[u] = rcoef ? rcoef[e] : __dmul_rn((double)rwt[e], __ldg(psi_b + m));
@@ -609,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                 const int64_t moff = b * a.ms + q;
                 const double* ub = u_in + b * a.ms;
                 const double* psi_b = a.psi + b * a.psi_stride;
+                FG_DCHECK(k < a.h_slices && k < a.psi_stride && q + 1 < a.ms + 1 && b < a.slice_stride / a.ms);
                 // every load of the C phase is issued before any arithmetic or
                 // store (one L2 round trip on the step chain's critical path)
                 const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
@@ -954,6 +985,8 @@ struct BlockArgs {
     const double* gcoef;  // precomputed coefficient rows (or NULL): single member, or
                           // itemized ensembles ([B][coef_mstride] per block buffer)
     int64_t coef_mstride; // doubles between members' coefficient rows (ensembles)
+    int64_t h_alloc;      // slices allocated at H (bounds checks)
+    int32_t tblock;       // rows of the P buffer (bounds checks)
 };
 
 // The history rows are moved by the bulk-copy engine (cp.async.bulk → shared
@@ -1055,11 +1088,11 @@ constexpr int kMainStages = FG_STAGED_RING;  // staged main launches
 #endif
 constexpr int kTailStages = FG_TAIL_STAGES;  // tail launches: small ring, so they fit beside two main CTAs per SM
 
-template <int BT, int TP, bool STAGED, int NS>
+template <int BT, int TP, bool STAGED, int NS, int WP>
 size_t tma_block_smem() {
     constexpr int CROWS = STAGED ? NS * kE : kCH;
     return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)CROWS * coef_pitch<BT>() * sizeof(double) +
-           (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double) +
+           (2 * NS) * sizeof(uint64_t) + (TP / WP) * sizeof(double) +
            (STAGED ? 0 : (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int));
 }
 
@@ -1105,6 +1138,7 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
         const int64_t i1 = (m_max - m0) / st < cnt - 1 ? (m_max - m0) / st : cnt - 1;
         for (int64_t i = i0 + threadIdx.x; i <= i1; i += blockDim.x) {
             const int64_t m = m0 + i * st;
+            FG_DCHECK(k - m >= ts && k - m < te && ((k - m - ts) + 1) * CP <= a.coef_mstride && m < a.psi_stride);
             out[(k - m - ts) * CP + bb] = __dmul_rn((double)st, __ldg(a.psi + m));
         }
     }
@@ -1118,14 +1152,23 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
 // Coefficients: single member → precomputed rows (fg_block_coef_kernel) copied
 // into the ring with each stage; ensembles (per-member ψ) → a kCH-slice table
 // rebuilt by the consumers at chunk boundaries (scatter over segments).
-template <int BT, int TP, bool STAGED, int NS>
-__global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+// WP: points per consumer warp (NT = WP/8 DMMA N tiles).  32-point warps share
+// each A fragment over 4 N tiles; 16-point warps hold half the accumulators, so
+// a CTA can have twice the warps (measured: the fp64 tensor pipe reaches its
+// peak only with 4 issuing warps per SM sub-partition, 16 per SM —
+// scripts/micro/dense_consumer.cu; 7-warp CTAs stop at 7/8 of it).
+template <int BT, int TP, bool STAGED, int NS, int WP>
+__global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
     constexpr int kStages = NS;
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
-    constexpr int NT = 4;       // N tiles of 8 points per warp (32 points)
-    constexpr int NW = TP / 32; // consumer warps
+    constexpr int NT = WP / 8;  // N tiles of 8 points per warp
+    constexpr int NW = TP / WP; // consumer warps
+    constexpr int NC = NW * 32; // consumer threads
+    // lean fragments (see the stage loop) for the 4-M-tile blocks: 96 instead of
+    // ~125 registers, so 8-warp CTAs (TP 256) fit two per SM
+    constexpr bool LEAN = MT == 4;
     constexpr int CROWS = STAGED ? kStages * kE : kCH;
     extern __shared__ __align__(128) unsigned char smem[];
     double* rows = reinterpret_cast<double*>(smem);                  // [kStages][kE][RP]
@@ -1179,6 +1222,9 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
                     const int64_t t0 = ts + gl * kE;
                     const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
                     const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
+                    FG_DCHECK(t0 >= 0 && t0 + nr <= a.h_alloc && t0 + nr <= a.kb0);
+                    FG_DCHECK(!staged || (t0 - ts + nr) * CP <= a.coef_mstride);
+                    FG_DCHECK(row_bytes <= TP * sizeof(double) && q0 + row_elems <= a.ms);
                     mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
                     for (int e = 0; e < nr; ++e)
                         bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
@@ -1193,9 +1239,9 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
     // ---- consumers: warp w owns points [32w, 32w+32) of the tile
     const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
     const double* psi_b = a.psi + mem * a.psi_stride;
-    const int ngroups = TP / BT;  // threads per step column when filling the table
+    const int ngroups = NC / BT;  // threads per step column when filling the table
     int64_t g = 0;
-    const uint32_t rows_s = smem_u32(rows) + (uint32_t)((warp * 32 + fr) * 8), coef_s = smem_u32(coef) + (uint32_t)(fr * 8);
+    const uint32_t rows_s = smem_u32(rows) + (uint32_t)((warp * WP + fr) * 8), coef_s = smem_u32(coef) + (uint32_t)(fr * 8);
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
     const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
     double d[MT][NT][2];
@@ -1209,9 +1255,9 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
         if (!staged && (gl * kE) % kCH == 0) {
             // ensemble path: coefficient table for slices t0 .. t0+kCH-1 — zero it,
             // then scatter w·ψ_b(m) over every schedule segment (no per-slice search)
-            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
-            for (int i = tid; i < kCH * CP; i += TP) coef[i] = 0.0;
-            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+            for (int i = tid; i < kCH * CP; i += NC) coef[i] = 0.0;
+            asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
             const int bb = tid % BT, grp = tid / BT;
             if (bb < a.bt && grp < ngroups) {
                 const int64_t k = a.kb0 + bb;
@@ -1229,13 +1275,38 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
                     }
                 }
             }
-            asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
         }
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
         const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
         const uint32_t rs = rows_s + (uint32_t)(s * kE * RP * 8);
         const uint32_t cs = staged ? coef_s + (uint32_t)(s * kE * CP * 8) : coef_s + (uint32_t)(((gl * kE) % kCH) * CP * 8);
+        if constexpr (LEAN) {
+        // one k-step (4 slices) of fragments live at a time, so 8 consumer warps
+        // of 32 points fit two CTAs per SM (the fp64 tensor pipe needs 16 issuing
+        // warps per SM, scripts/micro/dense_consumer.cu); the previous stage's slot
+        // is released after the first k-step's DMMAs: the dependency is on a DMMA
+        // issued after every DMMA that read the slot (so those reads are done),
+        // and 16 DMMAs old by the time the release needs it
+#pragma unroll
+        for (int ks = 0; ks < kE / 4; ++ks) {
+            const int e = ks * 4 + fk;
+            double af[MT], bf[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) af[i] = e < nr ? lds_f64(cs + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bf[j] = e < nr ? lds_f64(rs + (uint32_t)((e * RP + 8 * j) * 8)) : 0.0;
+            if (ks == 1) {
+                if (pend && lane == 0) mbar_arrive_after(pend, d[0][0][0], sink + warp);
+                pend = &empty[s];
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
+        }
+        } else {
         // all fragments of the stage into registers first (partial last stage masked) ...
         double af[kE / 4][MT], bf[kE / 4][NT];
 #pragma unroll
@@ -1258,18 +1329,20 @@ __global__ void __launch_bounds__(TP + 32, 2) fg_block_tma_kernel(const BlockArg
             for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
+        }
     }
     // the tile's last stage: released once its DMMAs are done (the flush needs them anyway)
     if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1], sink + warp);
     // D fragment: row = step fr (+8 per M tile), columns = 2 adjacent points
-    double* pout = a.P + mem * a.ms + q0 + warp * 32 + fk * 2;
+    double* pout = a.P + mem * a.ms + q0 + warp * WP + fk * 2;
+    FG_DCHECK(a.bt <= a.tblock && a.bt <= BT);
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         const int bb = 8 * i + fr;
         if (bb >= a.bt) continue;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-            const int64_t q = q0 + warp * 32 + 8 * j + fk * 2;
+            const int64_t q = q0 + warp * WP + 8 * j + fk * 2;
             if (q >= a.n_m) continue;
             double* o = pout + bb * a.slice_stride + 8 * j;
             if (a.accumulate) {
@@ -1364,6 +1437,7 @@ __global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ I
             w = fg_seg_weight(segs[c], nseg[c], m);
         }
         const bool on = w == it.stride;
+        FG_DCHECK(((int64_t)it.coef_row + j + 1) * CP <= a.coef_mstride && (!on || (m >= 1 && m < a.psi_stride)));
         double* o = out + ((int64_t)it.coef_row + j) * CP + c;
         for (int64_t mem = blockIdx.z; mem < n_members; mem += gridDim.z)
             o[mem * a.coef_mstride] = on ? __dmul_rn((double)w, __ldg(a.psi + mem * a.psi_stride + m)) : 0.0;
@@ -1463,6 +1537,8 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
                     if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
                     const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
                     const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
+                    FG_DCHECK(it.t_first + (j0 + nr - 1) * it.stride < a.h_alloc && it.t_first >= 0);
+                    FG_DCHECK(((int64_t)it.coef_row + j0 + nr) * CP <= a.coef_mstride);
                     mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
                     for (int e = 0; e < nr; ++e)
                         bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (j0 + e) * sstride, row_bytes,
@@ -1520,6 +1596,7 @@ __global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leav
         for (int i = 0; i < MT; ++i) {
             const int r = 8 * i + fr;
             if (i >= mt || r >= it.ncols) continue;
+            FG_DCHECK(it.col2step[r] < a.bt && a.bt <= a.tblock);
             double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
             const bool add = T.accumulate || !((it.first_mask >> r) & 1);
 #pragma unroll
@@ -1676,6 +1753,13 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
                         const int nr = (int)((it.n_slices - j0) < kIR ? (it.n_slices - j0) : kIR);
                         if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
                         const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
+                        // the box reads kIR slices of the progression: all of them allocated
+                        FG_DCHECK(it.t_first + (j0 + kIR - 1) * (int64_t)it.stride < a.h_alloc && it.t_first >= 0);
+                        FG_DCHECK(it.t_first + (j0 + nr - 1) * (int64_t)it.stride < a.kb0 + a.bt);
+                        FG_DCHECK(((int64_t)it.coef_row + j0 + nr) * CP <= a.coef_mstride);
+                        // a box may run past the member (partial last tile: its points are never
+                        // stored) or past the history (the TMA zero-fills); it starts inside
+                        FG_DCHECK(it.map < kMaxMaps && chunk0 < a.slice_stride / 16);
                         mbar_expect_tx(&full[s], (uint32_t)SB + cbytes);
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
@@ -1770,6 +1854,7 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
         for (int i = 0; i < MT; ++i) {
             const int r = 8 * i + fr;
             if (i >= mt || r >= it.ncols) continue;
+            FG_DCHECK(it.col2step[r] < a.bt && a.bt <= a.tblock);
             double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
             const bool add = T.accumulate || !((it.first_mask >> r) & 1);
 #pragma unroll
@@ -2010,6 +2095,8 @@ StepArgs make_args(const fg_plan* p, int s) {
     a.tpm = (int32_t)((p->n_m + tp - 1) / tp);
     a.total_tiles = (int32_t)(a.tpm * p->B);
     a.m0_from_history = (p->step_flags & FG_STEP_M0_FROM_HISTORY) ? 1 : 0;
+    a.h_slices = p->h_slices;
+    a.tblock = p->tblock;
     return a;
 }
 
@@ -2181,15 +2268,22 @@ struct BlockVariant {
     BlockKernel kern;
     size_t smem;
     int tp;
+    int threads;
 };
+
+template <int BT, int TP, bool ST, int NS, int WP>
+BlockVariant block_variant_tp() {
+    return {fg_block_tma_kernel<BT, TP, ST, NS, WP>, tma_block_smem<BT, TP, ST, NS, WP>(), TP, TP / WP * 32 + 32};
+}
 
 template <int BT, bool ST, int NS>
 BlockVariant block_variant(int tp) {
+    constexpr int WP = 32;  // 16-point warps at TP 128 measured slower (c4-full 1.58 vs 1.41 s)
     switch (tp) {
-        case 128: return {fg_block_tma_kernel<BT, 128, ST, NS>, tma_block_smem<BT, 128, ST, NS>(), 128};
-        case 192: return {fg_block_tma_kernel<BT, 192, ST, NS>, tma_block_smem<BT, 192, ST, NS>(), 192};
-        case 224: return {fg_block_tma_kernel<BT, 224, ST, NS>, tma_block_smem<BT, 224, ST, NS>(), 224};
-        default: return {fg_block_tma_kernel<BT, 256, ST, NS>, tma_block_smem<BT, 256, ST, NS>(), 256};
+        case 128: return block_variant_tp<BT, 128, ST, NS, WP>();
+        case 192: return block_variant_tp<BT, 192, ST, NS, WP>();
+        case 224: return block_variant_tp<BT, 224, ST, NS, WP>();
+        default: return block_variant_tp<BT, 256, ST, NS, WP>();
     }
 }
 
@@ -2207,21 +2301,21 @@ BlockVariant block_variant_of(bool staged, bool tail, int tp) {
 BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
     const int cands[4] = {256, 224, 192, 128};
     const bool staged = p->B == 1 && p->blkcoef_dev;
-    BlockVariant best = {nullptr, 0, 0};
-    auto usable = [&](int tp) { return !(p->tblock == 32 && tp == 256); };  // 32 x 256 spills
+    BlockVariant best = {nullptr, 0, 0, 0};
     auto cost_of = [&](int tp) {
         const int64_t tiles = ((p->n_m + tp - 1) / tp) * p->B;
         return ((tiles + sm_count() - 1) / sm_count()) * tp;
     };
     int64_t min_cost = INT64_MAX;
     for (int tp : cands)
-        if (usable(tp) && cost_of(tp) < min_cost) min_cost = cost_of(tp);
+        if (cost_of(tp) < min_cost) min_cost = cost_of(tp);
     // the widest tile within 2 % of the best balance: a wider CTA shares its
     // stage barrier and coefficient rows over more warps (measured c3-full at
-    // tblock 32: TP 224 705 ms vs TP 192 792 ms, nearly equal balance)
+    // tblock 32: TP 224 705 ms vs TP 192 792 ms, nearly equal balance; TP 256,
+    // 16 consumer warps per SM: 662 vs 678 ms at TP 224, c4-full 1386 vs 1411 ms)
     bool found = false;
     for (int tp : cands) {
-        if (!usable(tp) || found) continue;
+        if (found) continue;
         if (cost_of(tp) * 50 <= min_cost * 51) {
             found = true;
             switch (p->tblock) {
@@ -2243,6 +2337,8 @@ unsigned block_grid(const fg_plan* p, int64_t total_tiles) {
     return (unsigned)(total_tiles < cap ? total_tiles : cap);
 }
 
+int64_t history_alloc(const fg_plan* p) { return p->h_alloc > p->h_slices ? p->h_alloc : p->h_slices; }
+
 BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& v) {
     BlockArgs a;
     memset(&a, 0, sizeof a);
@@ -2262,6 +2358,8 @@ BlockArgs block_args(const fg_plan* p, int64_t kb0, int bt, const BlockVariant& 
     a.total_tiles = (int32_t)(a.tpm * p->B);
     a.gcoef = p->blkcoef_dev ? block_coef(p, kb0) : nullptr;
     a.coef_mstride = coef_capacity(p);
+    a.h_alloc = history_alloc(p);
+    a.tblock = p->tblock;
     return a;
 }
 
@@ -2504,7 +2602,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-int64_t history_alloc(const fg_plan* p) { return p->h_alloc > p->h_slices ? p->h_alloc : p->h_slices; }
 
 // Tensor maps of the table's strides (ItemMaps) and each item's map index.  A
 // stage box reads kE slices of the item's progression, so its last stage may
@@ -2688,7 +2785,7 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
     ++g_launches;
-    v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
+    v.kern<<<block_grid(p, a.total_tiles), v.threads, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
 
@@ -2721,7 +2818,7 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
     ++g_launches;
-    v.kern<<<block_grid(p, a.total_tiles), v.tp + 32, v.smem, st>>>(a);
+    v.kern<<<block_grid(p, a.total_tiles), v.threads, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
 
