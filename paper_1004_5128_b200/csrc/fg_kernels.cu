@@ -1404,6 +1404,8 @@ struct ItemTable {
 constexpr int kMaxMaps = 16;
 struct ItemMaps {
     CUtensorMap map[kMaxMaps];
+    CUtensorMap half[kMaxMaps];  // the same views with boxes of kIR/2 slices: an item's
+                                 // last stage of <= kIR/2 slices reads no more than it uses
 };
 
 // Coefficient rows of every item: row (coef_row + j), column c =
@@ -1760,10 +1762,14 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
                         // a box may run past the member (partial last tile: its points are never
                         // stored) or past the history (the TMA zero-fills); it starts inside
                         FG_DCHECK(it.map < kMaxMaps && chunk0 < a.slice_stride / 16);
-                        mbar_expect_tx(&full[s], (uint32_t)SB + cbytes);
+                        // a short last stage takes the half-depth boxes: they land on the
+                        // first kIR/2 rows of the same box slots (the consumers never read past nr)
+                        const bool half = nr <= kIR / 2;
+                        const CUtensorMap* mp = half ? &M.half[it.map] : map;
+                        mbar_expect_tx(&full[s], (uint32_t)(half ? SB / 2 : SB) + cbytes);
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
-                            tma_load_4d(rows + (size_t)s * SB + b * BOXB, map, 0, chunk0 + b * C, r,
+                            tma_load_4d(rows + (size_t)s * SB + b * BOXB, mp, 0, chunk0 + b * C, r,
                                         j_first + (int)j0, &full[s], pol);
                         bulk_g2s(coef + (size_t)s * kIR * CP, c0 + j0 * CP, cbytes, &full[s]);
                     }
@@ -2633,9 +2639,14 @@ int encode_item_maps(const fg_plan* p, ItemTable& T, int tp, ItemMaps& M) {
             const cuuint32_t box[4] = {16, (cuuint32_t)(tp == 96 ? item_box_chunks<96>() : item_box_chunks<128>()),
                                        1, (cuuint32_t)kIR};
             const cuuint32_t estride[4] = {1, 1, 1, 1};
-            const CUresult r = enc(&M.map[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, box,
-                                   estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CUresult r = enc(&M.map[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, box,
+                             estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            const cuuint32_t hbox[4] = {box[0], box[1], 1, (cuuint32_t)(kIR / 2)};
+            if (r == CUDA_SUCCESS)
+                r = enc(&M.half[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, hbox, estride,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(FG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for stride %lld", (int)r, (long long)s);
         }
