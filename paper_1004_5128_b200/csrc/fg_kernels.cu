@@ -1404,8 +1404,8 @@ struct ItemTable {
 constexpr int kMaxMaps = 16;
 struct ItemMaps {
     CUtensorMap map[kMaxMaps];
-    CUtensorMap half[kMaxMaps];  // the same views with boxes of kIR/2 slices: an item's
-                                 // last stage of <= kIR/2 slices reads no more than it uses
+    CUtensorMap half[kMaxMaps];     // the same views with boxes of kIR/2 and kIR/4 slices: an
+    CUtensorMap quarter[kMaxMaps];  // item's short last stage reads its rows rounded up to kIR/4
 };
 
 // Coefficient rows of every item: row (coef_row + j), column c =
@@ -1762,15 +1762,21 @@ __global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside tw
                         // a box may run past the member (partial last tile: its points are never
                         // stored) or past the history (the TMA zero-fills); it starts inside
                         FG_DCHECK(it.map < kMaxMaps && chunk0 < a.slice_stride / 16);
-                        // a short last stage takes the half-depth boxes: they land on the
-                        // first kIR/2 rows of the same box slots (the consumers never read past nr)
-                        const bool half = nr <= kIR / 2;
-                        const CUtensorMap* mp = half ? &M.half[it.map] : map;
-                        mbar_expect_tx(&full[s], (uint32_t)(half ? SB / 2 : SB) + cbytes);
+                        // a short last stage is covered by half- and quarter-depth boxes
+                        // (rows rounded up to kIR/4), landing on the same rows of the box
+                        // slots as the full box would (the consumers never read past nr)
+                        const int rows_rd = nr == kIR ? kIR : nr > kIR / 2 + kIR / 4 ? kIR : (nr + kIR / 4 - 1) / (kIR / 4) * (kIR / 4);
+                        mbar_expect_tx(&full[s], (uint32_t)(SB / kIR * rows_rd) + cbytes);
+                        for (int e0 = 0; e0 < rows_rd;) {
+                            const int depth = rows_rd - e0 >= kIR ? kIR : rows_rd - e0 >= kIR / 2 ? kIR / 2 : kIR / 4;
+                            const CUtensorMap* mp = depth == kIR ? map : depth == kIR / 2 ? &M.half[it.map]
+                                                                                          : &M.quarter[it.map];
 #pragma unroll
-                        for (int b = 0; b < NB; ++b)
-                            tma_load_4d(rows + (size_t)s * SB + b * BOXB, mp, 0, chunk0 + b * C, r,
-                                        j_first + (int)j0, &full[s], pol);
+                            for (int b = 0; b < NB; ++b)
+                                tma_load_4d(rows + (size_t)s * SB + b * BOXB + e0 * C * 128, mp, 0, chunk0 + b * C, r,
+                                            j_first + (int)j0 + e0, &full[s], pol);
+                            e0 += depth;
+                        }
                         bulk_g2s(coef + (size_t)s * kIR * CP, c0 + j0 * CP, cbytes, &full[s]);
                     }
                 }
@@ -2642,11 +2648,12 @@ int encode_item_maps(const fg_plan* p, ItemTable& T, int tp, ItemMaps& M) {
             CUresult r = enc(&M.map[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, box,
                              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            const cuuint32_t hbox[4] = {box[0], box[1], 1, (cuuint32_t)(kIR / 2)};
-            if (r == CUDA_SUCCESS)
-                r = enc(&M.half[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims, gstride, hbox, estride,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            for (int h = 0; h < 2 && r == CUDA_SUCCESS; ++h) {
+                const cuuint32_t hbox[4] = {box[0], box[1], 1, (cuuint32_t)(kIR / (2 << h))};
+                r = enc(h ? &M.quarter[m] : &M.half[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)p->H_dev, dims,
+                        gstride, hbox, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            }
             if (r != CUDA_SUCCESS)
                 return fail(FG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for stride %lld", (int)r, (long long)s);
         }
