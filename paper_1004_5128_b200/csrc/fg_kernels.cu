@@ -563,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                                              : make_double2(0.0, 0.0);  // its only read
                 FG_DCHECK(bb >= 0 && bb < a.tblock && k < a.h_slices && rn <= bb);
                 if (q < a.n_m && rn > 0) {
+                    const uint64_t pol_drop = l2_policy_first();
                     const double* hbase = a.H + b * a.ms + q + k * a.slice_stride;
                     const double* psi_b = a.psi + b * a.psi_stride;
                     const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
@@ -583,7 +584,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                             const bool on = e >= 0 && m <= mmax;
                             FG_DCHECK(!on || (m >= 2 && m <= k));
                             if (on) {
-                                v[u] = ld_stream(hbase - (int64_t)m * a.slice_stride);
+                                // evict_first: keeping even the newest slices in L2 (offsets
+                                // <= 3, 5 or 9 evict_last) measured slower than streaming them
+                                // (c4-adaptive 589 vs 599-610 ms): the L2 serves the rest better
+                                v[u] = ld_cg2_hint(hbase - (int64_t)m * a.slice_stride, pol_drop);
                                 c[u] = rcoef ? rcoef[e] : __dmul_rn((double)rwt[e], __ldg(psi_b + m));
                             } else {
                                 v[u] = make_double2(0.0, 0.0);
