@@ -124,6 +124,12 @@ __device__ __forceinline__ uint64_t l2_policy_last() {
     return pol;
 }
 
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __device__ __forceinline__ uint64_t l2_policy_first() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -324,6 +330,7 @@ struct StepArgs {
     const double* P;       // [tblock][B*ms] block partial sums (fg_block_kernel)
     int64_t h_slices;      // history capacity (bounds checks)
     int32_t tblock;        // rows of P (bounds checks)
+    int32_t recent_first;  // recent slices loaded evict_first (large fields)
     // blocked single-step launches: the entries of step k's schedule with
     // 2 <= m <= k-kb0 (the only ones a blocked step still sums itself), host-
     // evaluated so the step kernel builds no schedule: offsets ascending, weights,
@@ -563,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                                              : make_double2(0.0, 0.0);  // its only read
                 FG_DCHECK(bb >= 0 && bb < a.tblock && k < a.h_slices && rn <= bb);
                 if (q < a.n_m && rn > 0) {
-                    const uint64_t pol_drop = l2_policy_first();
+                    const uint64_t pol_drop = a.recent_first ? l2_policy_first() : l2_policy_normal();
                     const double* hbase = a.H + b * a.ms + q + k * a.slice_stride;
                     const double* psi_b = a.psi + b * a.psi_stride;
                     const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
@@ -584,9 +591,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __g
                             const bool on = e >= 0 && m <= mmax;
                             FG_DCHECK(!on || (m >= 2 && m <= k));
                             if (on) {
-                                // evict_first: keeping even the newest slices in L2 (offsets
-                                // <= 3, 5 or 9 evict_last) measured slower than streaming them
-                                // (c4-adaptive 589 vs 599-610 ms): the L2 serves the rest better
+                                // large fields: evict_first — keeping even the newest slices in
+                                // L2 (offsets <= 3, 5 or 9 evict_last) measured slower than
+                                // streaming them (c4-adaptive 589 vs 599-610 ms); small fields'
+                                // recent slices stay in L2 (c2)
                                 v[u] = ld_cg2_hint(hbase - (int64_t)m * a.slice_stride, pol_drop);
                                 c[u] = rcoef ? rcoef[e] : __dmul_rn((double)rwt[e], __ldg(psi_b + m));
                             } else {
@@ -2113,6 +2121,7 @@ StepArgs make_args(const fg_plan* p, int s) {
     a.m0_from_history = (p->step_flags & FG_STEP_M0_FROM_HISTORY) ? 1 : 0;
     a.h_slices = p->h_slices;
     a.tblock = p->tblock;
+    a.recent_first = p->B * p->ms * (int64_t)sizeof(double) >= (int64_t)(4 << 20);
     return a;
 }
 
