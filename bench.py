@@ -453,7 +453,9 @@ def run_ours(args) -> None:
             for r in runs]
     cfgs = [r.cfg for r in runs]
     flags = None if args.flags is None else int(args.flags)
-    del runs  # free the resident histories before the public-API runs allocate theirs
+    # free the resident histories before the public-API runs allocate theirs (the
+    # loops above leave `r` bound to the last run: c5 cannot hold two histories)
+    del runs, r
     torch.cuda.empty_cache()
 
     # end to end through the public API, host arrays in and out (one untimed pass
