@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FGB200_ABI_VERSION 5
+#define FGB200_ABI_VERSION 6
 
 #define FG_OK 0
 #define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
@@ -112,6 +112,9 @@ typedef struct fg_plan {
     double* pair_dev;            /* [B*ms + 1] caller scratch of fused step pairs (1D/2D
                                     blocked runs): a field buffer, then the int64 step
                                     whose field it holds; NULL disables pairs       */
+    int64_t subdelay;            /* sub-block launches: sub-block i feeds the steps b >=
+                                    (i+1)*subblock + subdelay (1..subblock; 0 = subblock),
+                                    which then sum themselves offsets < subblock + subdelay */
 } fg_plan;
 
 /* fg_plan.step_flags: take the m = 0 term from the stored H[k] instead of

@@ -204,6 +204,26 @@ def default_subblock(p: "Problem", tblock: int) -> int:
     return s
 
 
+def default_subdelay(p: "Problem", subblock: int) -> int:
+    """Steps a sub-block launch has to finish (fg_plan.subdelay, 0 = one whole
+    sub-block): sub-block i feeds the steps from (i+1)·S + D on, so the steps
+    themselves sum offsets < S + D.  FGB200_SUBDELAY overrides."""
+    env = os.environ.get("FGB200_SUBDELAY")
+    if env is not None:
+        d = int(env)
+    elif p.kind == "adaptive":
+        # a quarter sub-block: measured on B200 (ms per run, D = S / 14 / 7 / 4 at
+        # S = 28): c4-adaptive 579 / 571 / 562 / 570, c3-adaptive 262 / 258 / 257 /
+        # 258, c5 (S = 32) 1128 / 1096 / 1088 / 1083 — the launch finishes in time
+        # and the steps sum ~4 fewer recent slices
+        d = subblock // 4
+    elif p.kind == "full":
+        d = subblock // 2  # c4-full (S = 8): 1342 / 1338 (D = 7) / 1317 (D = 4)
+    else:
+        d = 0
+    return d if 0 <= d <= subblock else 0
+
+
 def history_pad(p: "Problem", tblock: int) -> int:
     """Slices allocated past H[n] for a blocked run (fg_history_pad): the 16-column
     item stage reads whole TMA boxes of 16 slices of a strided progression (the
@@ -580,6 +600,7 @@ class Stepper:
 
         if plan.tblock and plan.blkcoef_dev and (p.kind == "adaptive" or B == 1):
             plan.subblock = default_subblock(p, int(plan.tblock))
+            plan.subdelay = default_subdelay(p, int(plan.subblock))
         self.tblock = int(plan.tblock)
         self.plan = plan
         self.k = 0

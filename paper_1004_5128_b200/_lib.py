@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FGB200_LIB") or os.path.join(HERE, "_lib", "libfgb200.so")
 
-ABI_VERSION = 5  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
+ABI_VERSION = 6  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
 FG_OK = 0
 FG_ERR_ARG = -1
 FG_ERR_CUDA = -2
@@ -83,6 +83,7 @@ class FgPlan(C.Structure):
         ("coef_rows", C.c_int64),
         ("h_alloc", C.c_int64),
         ("pair_dev", C.c_void_p),
+        ("subdelay", C.c_int64),
     ]
 
 

@@ -2018,6 +2018,8 @@ int validate_plan(const fg_plan* p) {
         return fail(FG_ERR_ARG,
                     "subblock must be 0, or divide tblock into at most %d parts (blkcoef_dev; adaptive or one member)",
                     kMaxSub);
+    if (p->subdelay < 0 || p->subdelay > p->subblock)
+        return fail(FG_ERR_ARG, "subdelay must be in [0, subblock]");
     if (p->tblock) {  // the block kernel keeps kBlkSegs segments per step
         FgSeg s[FG_MAX_SEGS];
         const int n = fg_segments(p->kind, p->h_slices, p->base, p->horizon_max > 0 ? p->horizon_max : 0, s);
@@ -2853,6 +2855,11 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
 
+// Steps of a block that sub-block i's launch feeds: b >= (i+1)S + D (D =
+// plan->subdelay, default S: the launch has one sub-block of steps to finish).
+int64_t sub_delay(const fg_plan* p) { return p->subdelay > 0 ? p->subdelay : p->subblock; }
+int64_t sub_first_step(const fg_plan* p, int i) { return (i + 1) * p->subblock + sub_delay(p); }
+
 // Sub-block launch (plan->subblock = S > 0): the slices of sub-block i of the
 // block kb0, [kb0 + iS, kb0 + (i+1)S), added into the P rows of the block's
 // steps b >= (i+2)S.  Those steps then sum themselves only the slices of their
@@ -2863,7 +2870,7 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
 // the block's buffer from row 0 (its tail and main launches are done).
 int launch_block_partial(const fg_plan* p, int64_t kb0, int bt, int i, cudaStream_t st) {
     const int64_t S = p->subblock;
-    const int b_lo = (int)((i + 2) * S);
+    const int b_lo = (int)sub_first_step(p, i);
     if (b_lo >= bt) return FG_OK;
     const BlockVariant v = choose_block_variant(p, true);
     if (!v.kern) return fail(FG_ERR_ARG, "no block-kernel variant for FGB200_BLOCK_TP");
@@ -3311,8 +3318,10 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
             // sub-blocks: slices older than the previous sub-block are in P already
             int64_t t_min = kb0;
             if (kb0 >= 0 && p->subblock > 0) {
-                const int64_t i = (k - kb0) / p->subblock;
-                t_min = kb0 + (i > 0 ? (i - 1) * p->subblock : 0);
+                // sub-blocks i with (i+1)S + D <= b are in P already: the step sums
+                // from the first one that is not (offsets < S + D)
+                const int64_t b = k - kb0, S = p->subblock, D = sub_delay(p);
+                t_min = kb0 + (b >= S + D ? S * ((b - D) / S) : 0);
             }
             if (int r = launch_single(p, k, snap, cap, wait, pdl, kb0, t_min)) return r;
             if (snap)
@@ -3360,16 +3369,33 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         }
         int r = FG_OK;
         for (int64_t k = ks; k < ke && r == FG_OK;) {
-            const int i = (int)((k - kb) / S);
-            const int64_t se = kb + (i + 1) * S < ke ? kb + (i + 1) * S : ke;
-            if (i >= 2 && pending[i - 2]) {
-                r = cuda_check(cudaStreamWaitEvent(cap, sdone[i - 2], 0), "sub-block join");
-                pending[i - 2] = false;
-                after_join = true;
+            const int64_t b = k - kb;
+            // this segment ends at the next sub-block end or the next join point
+            // (the first step a pending launch feeds), whichever comes first
+            int64_t se = kb + (b / S + 1) * S;
+            int join = -1;
+            for (int i = 0; i < kMaxSub; ++i)
+                if (pending[i]) {
+                    const int64_t fs = kb + sub_first_step(p, i);
+                    if (fs <= k) {
+                        join = i;
+                    } else if (fs < se) {
+                        se = fs;
+                    }
+                }
+            if (se > ke) se = ke;
+            if (join >= 0) {  // launches feeding this step (at most the oldest pending ones)
+                for (int i = 0; i <= join && r == FG_OK; ++i)
+                    if (pending[i] && kb + sub_first_step(p, i) <= k) {
+                        r = cuda_check(cudaStreamWaitEvent(cap, sdone[i], 0), "sub-block join");
+                        pending[i] = false;
+                        after_join = true;
+                    }
             }
             if (r == FG_OK) r = steps(k, se, kb, after_join);
             after_join = false;
-            if (r == FG_OK && se == kb + (i + 1) * S && (i + 2) * S < bt) {  // sub-block i is complete
+            const int i = (int)((se - 1 - kb) / S);
+            if (r == FG_OK && se == kb + (i + 1) * S && sub_first_step(p, i) < bt) {  // sub-block i is complete
                 r = cuda_check(cudaEventRecord(sready, cap), "sub-block fork");
                 if (r == FG_OK) r = cuda_check(cudaStreamWaitEvent(sstream, sready, 0), "sub-block fork wait");
                 if (r == FG_OK) r = launch_block_partial(p, kb, bt, i, sstream);

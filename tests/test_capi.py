@@ -26,7 +26,7 @@ def declared_functions():
 def test_library_exists_and_loads():
     assert os.path.exists(_lib.LIB_PATH), "run __graft_entry__.build() first"
     L = _lib.load()
-    assert L.fg_abi_version() == _lib.ABI_VERSION == 5
+    assert L.fg_abi_version() == _lib.ABI_VERSION == 6
 
 
 def test_every_declared_symbol_is_exported():
@@ -136,6 +136,11 @@ def test_blocking_fields_validated_without_gpu():
     assert run() == _lib.FG_ERR_ARG
     plan.subblock = 32
     assert run() == _lib.FG_OK
+    plan.subdelay = 33  # a sub-block launch feeds steps (i+1)S + D on, D <= S
+    assert run() == _lib.FG_ERR_ARG
+    plan.subdelay = 8
+    assert run() == _lib.FG_OK
+    plan.subdelay = 0
     plan.kind = 0  # dense memory: single member only
     plan.tblock, plan.subblock = 32, 8
     assert run() == _lib.FG_OK
