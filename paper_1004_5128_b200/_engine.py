@@ -211,14 +211,14 @@ def default_subdelay(p: "Problem", subblock: int) -> int:
     env = os.environ.get("FGB200_SUBDELAY")
     if env is not None:
         d = int(env)
-    elif p.kind == "adaptive":
+    elif p.kind in ("adaptive", "full"):
         # a quarter sub-block: measured on B200 (ms per run, D = S / 14 / 7 / 4 at
         # S = 28): c4-adaptive 579 / 571 / 562 / 570, c3-adaptive 262 / 258 / 257 /
-        # 258, c5 (S = 32) 1128 / 1096 / 1088 / 1083 — the launch finishes in time
-        # and the steps sum ~4 fewer recent slices
+        # 258, c5 (S = 32) 1128 / 1096 / 1088 / 1083; c4-full (S = 8, D = 8 / 4 / 2)
+        # 1342 / 1317 / 1312 — the launch still finishes in time and the steps sum
+        # fewer recent slices.  Short memory (S = 4) keeps D = S (c3-short 247 vs
+        # 267 at D = 2).
         d = subblock // 4
-    elif p.kind == "full":
-        d = subblock // 2  # c4-full (S = 8): 1342 / 1338 (D = 7) / 1317 (D = 4)
     else:
         d = 0
     return d if 0 <= d <= subblock else 0
