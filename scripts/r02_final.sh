@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 final measurement pass on one B200 (gpurun, from the repo root): GPU suite with the
 # config-scale parity log, smoke, default bench (c4) + reference arm, every other config, launch list.
-O=gpurun_out/r02f
+O=${OUT:-gpurun_out/r02f}
 mkdir -p $O
 nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv > $O/gpu.txt; nproc >> $O/gpu.txt; free -g >> $O/gpu.txt
 FGB200_PARITY_LOG=$O/parity.jsonl timeout 2400 python -m pytest tests -q -m gpu -rs > $O/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 $O/pytest_gpu.log

@@ -441,16 +441,21 @@ def test_item_widths_match_goldens(fg, golden, name, cols, monkeypatch):
         test_temporal_blocking_matches_goldens(fg, golden, name, tb)
 
 
-@pytest.mark.parametrize("sub,tb,cols", [("8", 64, None), ("16", 128, None), ("32", 128, None), ("8", 32, None),
-                                         ("4", 24, None), ("28", 112, "16"), ("32", 128, "16")])
+@pytest.mark.parametrize("sub,tb,cols,delay", [("8", 64, None, None), ("16", 128, None, None), ("32", 128, None, None),
+                                               ("8", 32, None, None), ("4", 24, None, None), ("28", 112, "16", None),
+                                               ("32", 128, "16", None), ("28", 112, "16", "28"), ("28", 112, "16", "1"),
+                                               ("8", 32, None, "8"), ("8", 32, None, "1")])
 @pytest.mark.parametrize("name", ["c2_small", "point_adaptive5", "batch_adaptive", "3d_sat_adaptive",
                                   "spread_g09_adaptive4", "c2_small_full", "c2_small_short", "point_full",
                                   "point_short100"])
-def test_subblock_launches_match_goldens(fg, golden, name, sub, tb, cols, monkeypatch):
+def test_subblock_launches_match_goldens(fg, golden, name, sub, tb, cols, delay, monkeypatch):
     """Sub-block launches (finished sub-blocks streamed into the later steps'
     partial sums on a third stream) reproduce the reference (<= 1e-10); (28,
-    112, 16-column items) is the default of single large adaptive fields (c3, c4)."""
+    112, 16-column items, delay 7) is the default of single large adaptive fields
+    (c3, c4); delays 1 and S bracket the default S/4."""
     monkeypatch.setenv("FGB200_SUBBLOCK", sub)
+    if delay:
+        monkeypatch.setenv("FGB200_SUBDELAY", delay)
     if cols:
         monkeypatch.setenv("FGB200_ITEM_COLS", cols)
     dense = name.endswith("full") or "short" in name
