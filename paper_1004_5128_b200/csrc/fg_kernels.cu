@@ -1706,7 +1706,9 @@ __device__ __forceinline__ void item_stage_sw(double (&d)[MT][NT][2], uint32_t c
         for (int j = 0; j < NT; ++j)  // rows past the item's end hold other (or unwritten) slices: masked
             bf[ks][j] = (FULL || e < nr) ? lds_f64(ra + boff[ks][j]) : 0.0;
     }
-    if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1] + d[0][NT - 1][1], sink_w);
+    // the previous stage of this item had the same MTE: its last DMMA wrote d[MTE - 1][NT - 1]
+    // (a register dependency only: an add here would take a slot of the fp64 pipe)
+    if (pend && lane == 0) mbar_arrive_after(pend, d[MTE - 1][NT - 1][1], sink_w);
 #pragma unroll
     for (int ks = 0; ks < kE / 4; ++ks)
 #pragma unroll
