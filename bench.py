@@ -24,7 +24,8 @@ host's cores) on exact prefixes of the same runs.
 ``--impl reference`` times that CPU reference arm alone (rank 0; other ranks exit).
 Under torchrun (N > 1) every rank runs an independently seeded replica of the
 workload (weak scaling; the spatial slab split of one field is
-``paper_1004_5128_b200.sharding``).
+``paper_1004_5128_b200.sharding``); ``--config c5`` instead splits
+one ensemble by member across the ranks (strong scaling, no collective).
 """
 
 from __future__ import annotations
@@ -63,6 +64,13 @@ FP64_TENSOR_PEAK = 37.0e12  # DMMA m8n8k4, measured on this pool (scripts/micro/
 
 def runs_of(name: str) -> tuple[str, ...]:
     return GROUPS.get(name, (name,))
+
+
+def sharded(name: str, world: int) -> bool:
+    """Multi-GPU c5: one 2048-member ensemble split by member across the ranks
+    (sharding.shard_config, no data-path collective); every other workload runs
+    one seeded replica per rank."""
+    return world > 1 and name == "c5"
 
 
 def workload(name: str, rank: int = 0):
@@ -310,11 +318,16 @@ def time_block_stage(st, prob, stream) -> dict:
 class Run:
     """One run of the workload: its stepper, resident u0 and accounting."""
 
-    def __init__(self, name, rank, dev, args):
+    def __init__(self, name, rank, dev, args, world=1):
         from paper_1004_5128_b200._engine import Stepper, execution_bytes
+        from paper_1004_5128_b200.sharding import shard_config
 
         self.name = name
-        self.cfg, self.desc = workload(name, rank)
+        if sharded(name, world):  # one ensemble, members split across the ranks
+            cfg, self.desc = workload(name, 0)
+            self.cfg = shard_config(cfg, rank, world)
+        else:  # one seeded replica per rank
+            self.cfg, self.desc = workload(name, rank)
         self.prob = self.cfg.to_problem()
         flags = None if args.flags is None else int(args.flags)
         self.st = Stepper(self.prob, device=dev, split=args.split, flags=flags, tblock=args.tblock)
@@ -366,7 +379,7 @@ def run_ours(args) -> None:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    runs = [Run(name, rank, dev, args) for name in runs_of(args.config)]
+    runs = [Run(name, rank, dev, args, world) for name in runs_of(args.config)]
     stream = torch.cuda.current_stream(dev)
     L = _lib.load()
     terms = sum(r.terms for r in runs)
@@ -484,11 +497,15 @@ def run_ours(args) -> None:
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if sharded(args.config, world) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": group_desc(args.config), "runs": info, "terms_per_step": terms,
                        "l2": "inputs larger than L2 (history > 126 MB L2; not flushed)",
-                       "parallelism": f"independent replicas x{world} (weak scaling)" if world > 1 else "single GPU",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"ensemble members sharded x{world} (strong scaling, no collective)"
+                                       if sharded(args.config, world) else
+                                       f"independent replicas x{world} (weak scaling)"),
                        "launch": launch_geo},
             "gpu_launches": total_launches,
             "roofline": roofline,

@@ -172,3 +172,18 @@ def test_gloo_slab_run_bitwise_equals_single_process(shape, kind, param, reactio
     ref = fo.run(fo.OracleProblem(u0=u0[None], gamma=np.array([gamma]), dt=np.array([dt]), alpha=1.0, dx=1.0,
                                   reaction=reaction, strategy=(kind, param), n_steps=n_steps))
     assert np.array_equal(out[0], ref["final"][0]) and np.array_equal(out[1], ref["final"][0])
+
+
+def test_bench_multi_gpu_c5_is_member_sharded():
+    """bench.py --gpus N --config c5 splits ONE seeded ensemble by member (strong
+    scaling): the ranks' shards are disjoint, cover all 2048 members, and keep
+    each member's γ, Δt and initial field; other workloads run replicas."""
+    import bench
+    from paper_1004_5128_b200.sharding import shard_config
+
+    assert bench.sharded("c5", 2) and not bench.sharded("c5", 1) and not bench.sharded("c4", 8)
+    cfg, _ = bench.workload("c5", 0)
+    parts = [shard_config(cfg, r, 3) for r in range(3)]
+    assert sum(p.members() for p in parts) == cfg.members()
+    np.testing.assert_array_equal(np.concatenate([np.asarray(p.gamma) for p in parts]), np.asarray(cfg.gamma))
+    np.testing.assert_array_equal(np.concatenate([np.asarray(p.initial) for p in parts]), np.asarray(cfg.initial))
