@@ -1100,10 +1100,16 @@ constexpr int kMainStages = FG_STAGED_RING;  // staged main launches
 #endif
 constexpr int kTailStages = FG_TAIL_STAGES;  // tail launches: small ring, so they fit beside two main CTAs per SM
 
+// slice rows per stage of the dense kernel: 16 for the 4-M-tile blocks (lean
+// consumers), kE otherwise; rings keep their bytes (fewer, deeper stages)
+template <int BT>
+__host__ __device__ constexpr int dense_ke() { return BT / 8 == 4 ? 16 : kE; }
+
 template <int BT, int TP, bool STAGED, int NS, int WP>
 size_t tma_block_smem() {
-    constexpr int CROWS = STAGED ? NS * kE : kCH;
-    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)CROWS * coef_pitch<BT>() * sizeof(double) +
+    constexpr int KE = dense_ke<BT>();
+    constexpr int CROWS = STAGED ? NS * KE : kCH;
+    return (size_t)NS * KE * row_pitch<TP>() * sizeof(double) + (size_t)CROWS * coef_pitch<BT>() * sizeof(double) +
            (2 * NS) * sizeof(uint64_t) + (TP / WP) * sizeof(double) +
            (STAGED ? 0 : (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int));
 }
@@ -1172,6 +1178,7 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
 template <int BT, int TP, bool STAGED, int NS, int WP>
 __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
     constexpr int kStages = NS;
+    constexpr int KE = dense_ke<BT>();  // slice rows per stage
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
@@ -1181,10 +1188,10 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
     // lean fragments (see the stage loop) for the 4-M-tile blocks: 96 instead of
     // ~125 registers, so 8-warp CTAs (TP 256) fit two per SM
     constexpr bool LEAN = MT == 4;
-    constexpr int CROWS = STAGED ? kStages * kE : kCH;
+    constexpr int CROWS = STAGED ? kStages * KE : kCH;
     extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);                  // [kStages][kE][RP]
-    double* coef = rows + kStages * kE * RP;                        // [CROWS][CP]
+    double* rows = reinterpret_cast<double*>(smem);                  // [kStages][KE][RP]
+    double* coef = rows + kStages * KE * RP;                        // [CROWS][CP]
     uint64_t* full = reinterpret_cast<uint64_t*>(coef + CROWS * CP);  // [kStages]
     uint64_t* empty = full + kStages;                               // [kStages]
     double* sink = reinterpret_cast<double*>(empty + kStages);      // [NW] release dependencies
@@ -1206,7 +1213,7 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
     const int64_t ts = a.t_begin > t_lo ? a.t_begin : t_lo;
     const int64_t te = a.t_end;
     const int64_t n_sl = te > ts ? te - ts : 0;
-    const int64_t n_st = (n_sl + kE - 1) / kE;
+    const int64_t n_st = (n_sl + KE - 1) / KE;
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -1231,17 +1238,17 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
                 for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
                     const int s = (int)(g % kStages);
                     if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                    const int64_t t0 = ts + gl * kE;
-                    const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
+                    const int64_t t0 = ts + gl * KE;
+                    const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
                     const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
                     FG_DCHECK(t0 >= 0 && t0 + nr <= a.h_alloc && t0 + nr <= a.kb0);
                     FG_DCHECK(!staged || (t0 - ts + nr) * CP <= a.coef_mstride);
                     FG_DCHECK(row_bytes <= TP * sizeof(double) && q0 + row_elems <= a.ms);
                     mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
                     for (int e = 0; e < nr; ++e)
-                        bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
+                        bulk_g2s_hint(rows + ((size_t)s * KE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
                                       &full[s], pol);
-                    if (staged) bulk_g2s(coef + (size_t)s * kE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
+                    if (staged) bulk_g2s(coef + (size_t)s * KE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
                 }
             }
         }
@@ -1263,8 +1270,8 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
     uint64_t* pend = nullptr;  // slot of the previous stage, released by the next one
     for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
-        const int64_t t0 = ts + gl * kE;
-        if (!staged && (gl * kE) % kCH == 0) {
+        const int64_t t0 = ts + gl * KE;
+        if (!staged && (gl * KE) % kCH == 0) {
             // ensemble path: coefficient table for slices t0 .. t0+kCH-1 — zero it,
             // then scatter w·ψ_b(m) over every schedule segment (no per-slice search)
             asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
@@ -1291,18 +1298,20 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         }
         const int s = (int)(g % kStages);
         mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
-        const int nr = (int)((te - t0) < kE ? (te - t0) : kE);
-        const uint32_t rs = rows_s + (uint32_t)(s * kE * RP * 8);
-        const uint32_t cs = staged ? coef_s + (uint32_t)(s * kE * CP * 8) : coef_s + (uint32_t)(((gl * kE) % kCH) * CP * 8);
+        const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
+        const uint32_t rs = rows_s + (uint32_t)(s * KE * RP * 8);
+        const uint32_t cs = staged ? coef_s + (uint32_t)(s * KE * CP * 8) : coef_s + (uint32_t)(((gl * KE) % kCH) * CP * 8);
         if constexpr (LEAN) {
         // one k-step (4 slices) of fragments live at a time, so 8 consumer warps
         // of 32 points fit two CTAs per SM (the fp64 tensor pipe needs 16 issuing
         // warps per SM, scripts/micro/dense_consumer.cu); the previous stage's slot
         // is released after the first k-step's DMMAs: the dependency is on a DMMA
         // issued after every DMMA that read the slot (so those reads are done),
-        // and 16 DMMAs old by the time the release needs it
-#pragma unroll
-        for (int ks = 0; ks < kE / 4; ++ks) {
+        // and 16 DMMAs old by the time the release needs it.  Stages of 16 slices
+        // (4 k-steps, not unrolled: registers) halve the barrier round trips per
+        // DMMA (c4-full 1310 -> 1277 ms, c3-full 633 -> 616)
+#pragma unroll 1
+        for (int ks = 0; ks < KE / 4; ++ks) {
             const int e = ks * 4 + fk;
             double af[MT], bf[NT];
 #pragma unroll
@@ -1320,9 +1329,9 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         }
         } else {
         // all fragments of the stage into registers first (partial last stage masked) ...
-        double af[kE / 4][MT], bf[kE / 4][NT];
+        double af[KE / 4][MT], bf[KE / 4][NT];
 #pragma unroll
-        for (int ks = 0; ks < kE / 4; ++ks) {
+        for (int ks = 0; ks < KE / 4; ++ks) {
             const int e = ks * 4 + fk;
 #pragma unroll
             for (int i = 0; i < MT; ++i) af[ks][i] = e < nr ? lds_f64(cs + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
@@ -1336,7 +1345,7 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1], sink + warp);
         pend = &empty[s];
 #pragma unroll
-        for (int ks = 0; ks < kE / 4; ++ks)
+        for (int ks = 0; ks < KE / 4; ++ks)
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -2323,7 +2332,8 @@ BlockVariant block_variant(int tp) {
 template <int BT>
 BlockVariant block_variant_of(bool staged, bool tail, int tp) {
     if (tail) return staged ? block_variant<BT, true, kTailStages>(tp) : block_variant<BT, false, kTailStages>(tp);
-    return staged ? block_variant<BT, true, kMainStages>(tp) : block_variant<BT, false, ring_stages<false>()>(tp);
+    constexpr int main_ns = kMainStages * kE / dense_ke<BT>(), ens_ns = ring_stages<false>() * kE / dense_ke<BT>();
+    return staged ? block_variant<BT, true, main_ns>(tp) : block_variant<BT, false, (ens_ns > 2 ? ens_ns : 2)>(tp);
 }
 
 // tail: the variant with the small ring (see kTailStages)
