@@ -1179,6 +1179,7 @@ template <int BT, int TP, bool STAGED, int NS, int WP>
 __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
     constexpr int kStages = NS;
     constexpr int KE = dense_ke<BT>();  // slice rows per stage
+    static_assert(KE < 32, "one producer lane per stage row, lane 31 copies the coefficient rows");
     constexpr int RP = row_pitch<TP>();
     constexpr int CP = coef_pitch<BT>();
     constexpr int MT = BT / 8;  // M tiles (steps)
@@ -1226,30 +1227,33 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
     __syncthreads();
 
-    if (warp == NW) {  // ---- producer: lane 0 drives the bulk-copy ring
-        if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            int64_t g = 0;  // stage counter over all tiles of the CTA
-            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-                const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
-                const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
-                const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
-                const double* src0 = a.H + mem * a.ms + q0;
-                for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
-                    const int s = (int)(g % kStages);
+    if (warp == NW) {  // ---- producer warp: lane 0 waits and arms the barrier, lane e copies row e
+        // (one warp instruction issues a stage's row copies: c4-full 1292 -> 1285 ms)
+        const uint64_t pol = l2_evict_first_policy();
+        int64_t g = 0;  // stage counter over all tiles of the CTA
+        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+            const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
+            const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+            const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+            const double* src0 = a.H + mem * a.ms + q0;
+            for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
+                const int s = (int)(g % kStages);
+                const int64_t t0 = ts + gl * KE;
+                const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
+                const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
+                if (lane == 0) {
                     if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                    const int64_t t0 = ts + gl * KE;
-                    const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
-                    const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
                     FG_DCHECK(t0 >= 0 && t0 + nr <= a.h_alloc && t0 + nr <= a.kb0);
                     FG_DCHECK(!staged || (t0 - ts + nr) * CP <= a.coef_mstride);
                     FG_DCHECK(row_bytes <= TP * sizeof(double) && q0 + row_elems <= a.ms);
                     mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
-                    for (int e = 0; e < nr; ++e)
-                        bulk_g2s_hint(rows + ((size_t)s * KE + e) * RP, src0 + (t0 + e) * a.slice_stride, row_bytes,
-                                      &full[s], pol);
-                    if (staged) bulk_g2s(coef + (size_t)s * KE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
                 }
+                __syncwarp();  // the slot is free (lane 0 waited) before any lane copies into it
+                if (lane < nr)
+                    bulk_g2s_hint(rows + ((size_t)s * KE + lane) * RP, src0 + (t0 + lane) * a.slice_stride, row_bytes,
+                                  &full[s], pol);
+                if (staged && lane == 31)
+                    bulk_g2s(coef + (size_t)s * KE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
             }
         }
         return;
