@@ -19,7 +19,9 @@ kernel (the block stage of the run with the most block-stage time: the dense
 fp64-tensor block kernel for full memory, the TMA item kernel for adaptive
 memory) against its measured peak; ``runs`` carries every run's own numbers.
 ``cpu_baseline`` is the C restatement of the reference (oracle/, OpenMP over the
-host's cores) on exact prefixes of the same runs.
+host's cores) on exact prefixes of the same runs.  ``other_configs`` (default
+workload, one GPU) adds a short device-timed line for every other BASELINE
+config (c1, c2, c3, c5: one warm + two timed complete runs each).
 
 ``--impl reference`` times that CPU reference arm alone (rank 0; other ranks exit).
 Under torchrun (N > 1) every rank runs an independently seeded replica of the
@@ -278,11 +280,25 @@ def run_reference(args) -> None:
 
 # ------------------------------------------------------------------ GPU arm --
 
-def time_block_stage(st, prob, stream) -> dict:
+def sub_launch_bytes(st, prob, bt: int) -> int:
+    """Algorithmic bytes of one block's sub-block launches: launch i reads its
+    S slices once and adds into the P rows of the steps b >= (i+1)S + D (a
+    read-modify-write of each row)."""
+    S = int(st.plan.subblock)
+    D = int(st.plan.subdelay) or S
+    rows = 0
+    i = 0
+    while (i + 1) * S + D < bt:
+        rows += S + 2 * (bt - ((i + 1) * S + D))
+        i += 1
+    return rows * prob.batch * prob.n_m * 8
+
+
+def time_block_stage(st, prob, stream, with_sub: bool = False) -> dict:
     """Every block-stage launch pair (main + tail) of one run, replayed over the
     resident history (left by the timed runs) between CUDA events on the
-    launching stream.  The sub-block launches of the real run (slices inside a
-    block) are not replayed and not counted."""
+    launching stream; ``with_sub`` also replays each block's sub-block launches
+    (slices inside the block, fg_block_subpartials) and counts their bytes."""
     import ctypes as C
 
     import torch
@@ -296,18 +312,33 @@ def time_block_stage(st, prob, stream) -> dict:
         return None
     h = C.c_void_p(_lib.stream_handle(stream))
     plan = C.byref(st.plan)
-    for kb0, bt, _, _ in blocks[-4:]:  # warm (code, smem config)
+    n_sub = C.c_int32(0)
+    sub_launches = 0
+
+    def stage(kb0, bt):
+        nonlocal sub_launches
         _lib.check(L.fg_block_partials(plan, kb0, bt, h), "fg_block_partials")
+        if with_sub:
+            _lib.check(L.fg_block_subpartials(plan, kb0, bt, h, C.byref(n_sub)), "fg_block_subpartials")
+            sub_launches += n_sub.value
+
+    for kb0, bt, _, _ in blocks[-4:]:  # warm (code, smem config)
+        stage(kb0, bt)
+    sub_launches = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
     for kb0, bt, _, _ in blocks:
-        _lib.check(L.fg_block_partials(plan, kb0, bt, h), "fg_block_partials")
+        stage(kb0, bt)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     nbytes = sum(b[2] for b in blocks)
     flops = sum(b[3] for b in blocks)
+    if with_sub:
+        nbytes += sum(sub_launch_bytes(st, prob, b[1]) for b in blocks)
+        return {"launches": len(blocks), "sub_block_launches": sub_launches, "total_ms": ms,
+                "alg_bytes_total": nbytes, "hbm_gbs": nbytes / (ms * 1e-3) / 1e9}
     return {"launches": len(blocks), "total_ms": ms, "avg_launch_us": ms * 1e3 / len(blocks),
             "alg_bytes_per_launch": nbytes / len(blocks), "alg_bytes_total": nbytes,
             "alg_flops_per_launch": flops / len(blocks), "alg_flops_total": flops,
@@ -362,8 +393,48 @@ class Run:
                 # past the fp64 tensor ridge (37 TF/s ÷ 6.45 TB/s ≈ 5.7 flop/B)
                 blk["bound"] = "tensor" if st.tblock * 2 / 8 > FP64_TENSOR_PEAK / (peak_gbs * 1e9) else "hbm"
             blk["hbm_frac"] = blk["hbm_gbs"] / peak_gbs
+            if int(st.plan.subblock) > 0 and prob.kind == "adaptive":
+                # the same item kernel also runs the block's sub-block launches: the
+                # whole stage (main + tail + sub-blocks) replayed serially
+                sub = time_block_stage(st, prob, stream, with_sub=True)
+                sub["hbm_frac"] = sub["hbm_gbs"] / peak_gbs
+                blk["with_sub_blocks"] = sub
         out["block_stage"] = blk
         return out
+
+
+OTHER_CONFIGS = ("c1", "c2", "c3", "c5")  # every other BASELINE config, a short line each
+
+
+def quick_line(name: str, rank: int, dev, args, stream, reps: int = 2) -> dict:
+    """Device-timed runs of another BASELINE config (same method as the headline:
+    inputs resident, CUDA events on the launching stream, one untimed warm run)."""
+    import torch
+
+    runs = [Run(r, rank, dev, args) for r in runs_of(name)]
+    for r in runs:
+        r.run()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(runs) + 1)] for _ in range(reps)]
+    for i in range(reps):
+        evs[i][0].record(stream)
+        for j, r in enumerate(runs):
+            r.run()
+            evs[i][j + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    for r in runs:
+        r.st.raise_if_diverged()
+    out = {"workload": group_desc(name), "reps": reps, "runs": {}}
+    tot_ms = 0.0
+    for j, r in enumerate(runs):
+        ms = statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(reps))
+        tot_ms += ms
+        out["runs"][r.name] = {"ms_per_run": ms, "terms_per_run": r.terms, "terms_per_s": r.terms / (ms * 1e-3),
+                               "temporal_block": r.st.tblock, "history_gb": (r.prob.n_steps + 1) * r.prob.batch * r.prob.n_m * 8 / 1e9}
+    out["value"] = sum(r.terms for r in runs) / (tot_ms * 1e-3)
+    out["unit"] = UNIT
+    out["ms_per_step"] = tot_ms
+    return out
 
 
 def run_ours(args) -> None:
@@ -487,6 +558,18 @@ def run_ours(args) -> None:
     e2e_max = max_over_ranks(e2e_local, dev)
     e2e_value = sum_over_ranks(float(terms), dev) / e2e_max
 
+    # the other BASELINE configs, a short device-timed line each (default workload only)
+    others = None
+    if world == 1 and args.config == "c4" and not args.no_other_configs and args.tblock is None:
+        others = {}
+        for name in OTHER_CONFIGS:
+            torch.cuda.empty_cache()
+            try:
+                others[name] = quick_line(name, rank, dev, args, stream)
+            except Exception as exc:  # the headline line must survive a failed side measurement
+                others[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         t, el, what = cpu_group(args.config, REF_PREFIX)
@@ -513,6 +596,7 @@ def run_ours(args) -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_max},
             "clocks": clocks,
+            "other_configs": others,
             "per_step_ms": per_step_ms,
             "device": torch.cuda.get_device_name(dev),
         }
@@ -532,6 +616,8 @@ def main(argv=None) -> None:
     ap.add_argument("--flags", type=int, default=None)
     ap.add_argument("--tblock", type=int, default=None, help="temporal blocking factor (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the short lines of the other BASELINE configs (default workload only)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FGB200_ABI_VERSION 6
+#define FGB200_ABI_VERSION 7
 
 #define FG_OK 0
 #define FG_ERR_ARG (-1)         /* invalid argument (maps to ValueError)          */
@@ -225,10 +225,6 @@ int fg_history_pad(int32_t kind, int64_t n_steps, int64_t base, int64_t* pad);
  * t < kb0 that the block of steps kb0..kb0+bt-1 reads (the union of their
  * schedules' old parts), i.e. the slices fg_block_kernel streams once. */
 int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t horizon, int64_t* count);
-/* Largest number of item coefficient rows (tail + main; 12 doubles each for
- * 8-column items, 20 for 16-column items) any temporal block of an n_steps run
- * needs: sizes blkcoef_dev for itemized ensembles (coef_rows >= ceil(rows *
- * pitch / 36)).  Host-only, no device work. */
 /* Host-only view of the item table the library builds for a temporal block
  * (steps kb0..kb0+bt-1, old slices [ts, te)): 20 int64 per item = t_first,
  * stride, n_slices, ncols, the ncols (<= 16) step columns (padded with -1).  *n_items =
@@ -237,6 +233,10 @@ int fg_block_union(int32_t kind, int64_t kb0, int32_t bt, int64_t base, int64_t 
 int fg_block_item_table(int32_t kind, int64_t kb0, int32_t bt, int64_t ts, int64_t te, int64_t base,
                         int64_t horizon, int32_t tblock, int32_t item_cols, int64_t* out, int32_t cap,
                         int32_t* n_items);
+/* Largest number of item coefficient rows (tail + main; 12 doubles each for
+ * 8-column items, 20 for 16-column items) any temporal block of an n_steps run
+ * needs: sizes blkcoef_dev for itemized ensembles (coef_rows >= ceil(rows *
+ * pitch / 36)).  Host-only, no device work. */
 int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t base, int64_t horizon,
                        int32_t item_cols, int64_t* max_rows);
 
@@ -246,6 +246,13 @@ int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t ba
  * launch (t < kb0 - tblock) followed by the tail launch (the rest).  Exposed
  * for testing the block kernel alone. */
 int fg_block_partials(const fg_plan* plan, int64_t kb0, int32_t bt, void* stream);
+/* The sub-block launches of the same block (plan->subblock = S > 0), one after
+ * the other on `stream`: sub-block i's slices [kb0 + iS, kb0 + (i+1)S) added
+ * into the P rows of the steps b >= (i+1)S + subdelay.  fg_run issues each one
+ * when its sub-block's steps are done; exposed so a measurement can replay a
+ * block's whole stage (main + tail + sub-blocks) over a resident history.
+ * *launched (optional) receives the number of sub-block launches issued. */
+int fg_block_subpartials(const fg_plan* plan, int64_t kb0, int32_t bt, void* stream, int32_t* launched);
 
 /* Launch geometry fg_step would use: CTAs, threads per CTA, split factor. */
 int fg_step_geometry(const fg_plan* plan, int64_t* ctas, int32_t* threads, int32_t* split);

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FGB200_LIB") or os.path.join(HERE, "_lib", "libfgb200.so")
 
-ABI_VERSION = 6  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
+ABI_VERSION = 7  # FGB200_ABI_VERSION of include/fgb200.h this binding mirrors
 FG_OK = 0
 FG_ERR_ARG = -1
 FG_ERR_CUDA = -2
@@ -36,7 +36,7 @@ REACTIONS = {"linear": 0, "saturating": 1}
 EXPORTS = (
     "fg_abi_version", "fg_plan_sizeof", "fg_last_error", "fg_kernel_launches", "fg_device_info", "fg_psi_tables", "fg_schedule_len",
     "fg_schedule_expand", "fg_history_sum", "fg_stencil", "fg_step", "fg_run", "fg_run_ex", "fg_status",
-    "fg_step_geometry", "fg_block_union", "fg_block_partials", "fg_block_item_rows",
+    "fg_step_geometry", "fg_block_union", "fg_block_partials", "fg_block_subpartials", "fg_block_item_rows",
     "fg_block_item_table", "fg_history_pad",
 )
 
@@ -113,6 +113,7 @@ def _declare(L):
         "fg_step_geometry": (C.c_int, [plan, _p64, _p32, _p32]),
         "fg_block_union": (C.c_int, [i32, i64, i32, i64, i64, _p64]),
         "fg_block_partials": (C.c_int, [plan, i64, i32, vp]),
+        "fg_block_subpartials": (C.c_int, [plan, i64, i32, vp, C.POINTER(C.c_int32)]),
         "fg_block_item_rows": (C.c_int, [i32, i64, i32, i64, i64, i32, _p64]),
         "fg_block_item_table": (C.c_int, [i32, i64, i32, i64, i64, i64, i64, i32, i32, _p64, i32, _p32]),
         "fg_history_pad": (C.c_int, [i32, i64, i64, _p64]),

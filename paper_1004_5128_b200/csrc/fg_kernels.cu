@@ -3556,6 +3556,18 @@ int fg_block_partials(const fg_plan* p, int64_t kb0, int32_t bt, void* stream) {
     return launch_block(p, kb0, bt, (cudaStream_t)stream);
 }
 
+int fg_block_subpartials(const fg_plan* p, int64_t kb0, int32_t bt, void* stream, int32_t* launched) {
+    if (int rc = validate_plan(p)) return rc;
+    if (!p->tblock || p->subblock <= 0) return fail(FG_ERR_ARG, "fg_block_subpartials: plan has no sub-block launches");
+    if (kb0 < 0 || bt < 1 || bt > p->tblock || kb0 + bt > p->psi_stride || kb0 + bt > p->h_slices)
+        return fail(FG_ERR_ARG, "fg_block_subpartials: block out of range");
+    int n = 0;
+    for (int i = 0; sub_first_step(p, i) < bt; ++i, ++n)
+        if (int rc = launch_block_partial(p, kb0, bt, i, (cudaStream_t)stream)) return rc;
+    if (launched) *launched = n;
+    return FG_OK;
+}
+
 int fg_block_item_rows(int32_t kind, int64_t n_steps, int32_t tblock, int64_t base, int64_t horizon,
                        int32_t item_cols, int64_t* max_rows) {
     if (item_cols != 8 && item_cols != 16) return fail(FG_ERR_ARG, "fg_block_item_rows: item_cols must be 8 or 16");

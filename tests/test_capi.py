@@ -26,7 +26,7 @@ def declared_functions():
 def test_library_exists_and_loads():
     assert os.path.exists(_lib.LIB_PATH), "run __graft_entry__.build() first"
     L = _lib.load()
-    assert L.fg_abi_version() == _lib.ABI_VERSION == 6
+    assert L.fg_abi_version() == _lib.ABI_VERSION == 7
 
 
 def test_every_declared_symbol_is_exported():

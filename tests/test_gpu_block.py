@@ -103,3 +103,55 @@ def test_ensemble_block_partials_match_numpy(cuda_device, n_pts, B, kb0, bt):
         want = expected_partials(Hs[:, b, :n_pts], "adaptive", 5, kb0, bt, table)
         scale = max(np.abs(want).max(), 1.0)
         assert np.abs(got[:, b, :n_pts] - want).max() <= 1e-12 * scale, f"member {b}"
+
+
+def expected_sub_partials(H, param, kb0, bt, S, D, table):
+    """Old part + what the sub-block launches add: launch i feeds the steps
+    b >= (i+1)S + D with the slices [kb0 + iS, kb0 + (i+1)S) their schedules use."""
+    from oracle import fg_oracle as fo
+
+    P = expected_partials(H, "adaptive", param, kb0, bt, table)
+    for b in range(bt):
+        offs, wts = fo.schedule("adaptive", kb0 + b, param, 1.0)
+        for m, w in zip(offs, wts):
+            t = kb0 + b - m
+            if t < kb0:
+                continue
+            i = (t - kb0) // S
+            if (i + 1) * S + D <= b:
+                P[b] += (w * table[m]) * H[t]
+    return P
+
+
+@pytest.mark.parametrize("shape", [(96, 96), (4100,)])
+@pytest.mark.parametrize("kb0,tblock,S,D", [(224, 112, 28, 7), (1024, 128, 32, 8), (640, 64, 16, 16), (1120, 112, 28, 28)])
+def test_subblock_partials_match_numpy(cuda_device, monkeypatch, shape, kb0, tblock, S, D):
+    """fg_block_subpartials replays a block's sub-block launches over a resident
+    history (bench.py's whole-stage replay): main + tail + sub-blocks against NumPy."""
+    import torch
+
+    import paper_1004_5128_b200 as fg
+    from paper_1004_5128_b200 import _lib
+    from paper_1004_5128_b200._engine import Stepper
+
+    bt = tblock
+    cfg = fg.FieldConfig(initial=np.zeros(shape), dx=1.0, gamma=0.58, dt=1.0, n_steps=kb0 + bt + 1,
+                         strategy=fg.AdaptiveMemory(5), history_byte_cap=None)
+    monkeypatch.setenv("FGB200_SUBBLOCK", str(S))
+    monkeypatch.setenv("FGB200_SUBDELAY", str(D))
+    st = Stepper(cfg.to_problem(), tblock=tblock)
+    assert int(st.plan.subblock) == S and (int(st.plan.subdelay) or S) == D
+    gen = torch.Generator(device=st.device).manual_seed(kb0 + S)
+    st.H.copy_(torch.randn(st.H.shape, generator=gen, device=st.device, dtype=torch.float64))
+    L = _lib.load()
+    n_sub = C.c_int32(-1)
+    for _ in range(2):  # rerun: the main launch overwrites P, so the result is the same
+        _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
+        _lib.check(L.fg_block_subpartials(C.byref(st.plan), kb0, bt, _lib.stream_handle(), C.byref(n_sub)))
+    torch.cuda.synchronize()
+    assert n_sub.value == len([i for i in range(bt // S) if (i + 1) * S + D < bt])
+    n = int(np.prod(shape))
+    H = st.H[: kb0 + bt, :n].cpu().numpy()
+    want = expected_sub_partials(H, 5, kb0, bt, S, D, st.psi[0].cpu().numpy())
+    got = st.block_partials(kb0)[:bt, :n].cpu().numpy()
+    assert np.abs(got - want).max() <= 1e-12 * max(np.abs(want).max(), 1.0)
