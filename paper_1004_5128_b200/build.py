@@ -19,7 +19,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libfgb200.so")
 SOURCES = [os.path.join(CSRC, "fg_kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "fg_schedule.cuh"), os.path.join(ROOT, "include", "fgb200.h")]
+HEADERS = ("fg_common.cuh", "fg_schedule.cuh", "fg_step.cuh", "fg_block_dense.cuh", "fg_block_items.cuh",
+           "fg_support.cuh")
+DEPS = SOURCES + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "fgb200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

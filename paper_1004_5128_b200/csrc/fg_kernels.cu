@@ -1,2000 +1,31 @@
-// B200 (sm_100a) kernels and the C ABI of the GL history stepper.
+// B200 (sm_100a) kernels and the C ABI of the GL history stepper — one translation unit.
 //
 // Hot path replaced: /root/reference/pkg/src/fracgrid/solver.py:230-265 (run)
 //   → step (:200-227) → history_sum (:162-197), with ψ from coefficients.py:76-92,
 //   schedules from schedule.py:70-151 and the stencil of grid.py:88-106.
 //
-// Design:
-//  * fg_step_kernel — the fused time step.  A CTA owns tiles of TP points (one
-//    member each).  Per step k:
-//      A  schedule of step k built in shared memory (segment table → slice index
-//         k-m and coefficient w·ψ_b(m), rounded once exactly like solver.py:190);
-//         every history slice with m >= 2 is streamed with 128-bit loads, 8 in
-//         flight per thread, fp64 FMA into per-tile partial sums.  When tiles are
-//         small the CTA's warps split the entry list S ways and combine in a
-//         fixed order (deterministic).
-//      -- dependency on step k-1 (grid barrier / griddepcontrol.wait) --
-//      C  m = 1 (H[k-1]) and m = 0 (δ^k = stencil(u^k), bit-exact, stored to H[k]),
-//         reaction + explicit update in the reference's rounding order, ring
-//         pinned to zero, non-finite detection, u^{k+1} (+ snapshot) stored.
-//    The same kernel runs one step per launch (fg_step, PDL/graph pipelines) or
-//    every step in one cooperative launch with a split arrive/wait grid barrier
-//    (FG_RUN_PERSISTENT): a CTA arrives after its C phase and only waits after
-//    streaming the next step's A phase, so the barrier latency hides under HBM
-//    traffic and there is no per-step launch or tail.  Same arithmetic in every
-//    mode → bitwise-identical results.
-//  * HBM-bound (0.25 flop/B): no tensor cores; roofline = 8 bytes per term.
-#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point, no -lcuda)
-#include <cuda_runtime.h>
-#include <cudaTypedefs.h>
-#include <stdarg.h>
-#include <stdint.h>
-#include <stdio.h>
-#include <string.h>
-
-#include <mutex>
-#include <string>
-#include <vector>
-
-#include "../../include/fgb200.h"
-#include "fg_schedule.cuh"
+// Layout:
+//   fg_common.cuh       error plumbing, constants, FG_CHECKS bounds checks, PTX helpers
+//   fg_schedule.cuh     schedule segments (host + device): full / short / adaptive
+//   fg_step.cuh         stencils, fg_step_kernel (one fused time step: recent-slice sum
+//                       before the dependency wait, then m = 1, m = 0 = stencil(u^k),
+//                       reaction + update in the reference's rounding order), fused pairs
+//   fg_block_dense.cuh  temporal blocking, dense stage: TMA ring + fp64 DMMA consumers
+//   fg_block_items.cuh  temporal blocking, itemized stage for thinned (adaptive) schedules
+//   fg_support.cuh      ψ tables, schedule expansion, standalone history_sum / stencil
+//   this file           host side: plan validation, kernel variants, launch pipeline
+//                       (PDL step chain, main/tail/sub-block launches, side streams,
+//                       graph capture, snapshots) and the C ABI of include/fgb200.h
+// A step reads 8 bytes of history per term (0.25 flop/B): unblocked it is HBM-bound;
+// the block stages read each old slice once per temporal block and run on the fp64
+// tensor pipe (DMMA m8n8k4), so full memory is fp64-bound and adaptive memory HBM-bound.
+#include "fg_common.cuh"
+#include "fg_step.cuh"
+#include "fg_block_dense.cuh"
+#include "fg_block_items.cuh"
+#include "fg_support.cuh"
 
 namespace {
-
-thread_local std::string g_last_error;
-thread_local int64_t g_launches = 0;  // kernels this thread has launched (fg_kernel_launches)
-
-int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
-int fail(int code, const char* fmt, ...) {
-    char buf[512];
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
-    va_end(ap);
-    g_last_error = buf;
-    return code;
-}
-
-int cuda_check(cudaError_t e, const char* what) {
-    if (e == cudaSuccess) return FG_OK;
-    return fail(FG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
-}
-
-// Device-side bounds checks (FG_CHECKS builds only; compute-sanitizer is closed
-// on the GPU pool): every global index a kernel derives from its launch
-// arguments — history slice, partial-sum row, coefficient row, tensor-map
-// coordinate, step column, ψ index — is checked against the buffer it
-// addresses, and a violation traps with file/line (scripts/checked_suite.sh runs
-// the GPU tests against that build).
-#ifdef FG_CHECKS
-#define FG_DCHECK(cond)                                                                                   \
-    do {                                                                                                  \
-        if (!(cond)) {                                                                                    \
-            printf("FG_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x,  \
-                   (int)threadIdx.x, #cond);                                                              \
-            __trap();                                                                                     \
-        }                                                                                                 \
-    } while (0)
-#else
-#define FG_DCHECK(cond) ((void)0)
-#endif
-
-constexpr int kThreads = 256;   // 8 warps
-#ifndef FG_STEP_MINB
-#define FG_STEP_MINB 4
-#endif
-constexpr int kMinBlocks = FG_STEP_MINB;   // resident CTAs per SM the register budget targets
-constexpr int kVec = 2;         // doubles per thread per slice (one 128-bit load)
-constexpr int kUnroll = 8;      // slices in flight per thread
-constexpr int kChunk = 1024;    // schedule entries staged in shared memory at once
-constexpr int kMaxPasses = 32;  // tiles per CTA in persistent mode (dynamic smem)
-#ifndef FG_MAX_TBLOCK
-#define FG_MAX_TBLOCK 128
-#endif
-constexpr int kMaxTBlock = FG_MAX_TBLOCK;  // largest temporal-blocking factor (> 32: itemized stages only)
-constexpr int kMaxSub = 16;      // most sub-blocks per temporal block (plan->subblock)
-constexpr int kMaxDenseTBlock = 32;  // largest factor of the dense block kernel
-constexpr int kCoefRow = 36;    // doubles per row of plan->blkcoef_dev (>= kMaxDenseTBlock + 4)
-
-// ---------------------------------------------------------------- PTX helpers ---
-
-// History slices: read once per step, never in L1 (.cg keeps the load coherent at
-// L2, which the persistent kernel needs because slices are written mid-launch).
-__device__ __forceinline__ double2 ld_stream(const double* p) {
-    double2 v;
-    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
-
-__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
-
-__device__ __forceinline__ double2 ld_cg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
-
-__device__ __forceinline__ void st_pair(double* p, double a, double b) {
-    *reinterpret_cast<double2*>(p) = make_double2(a, b);
-}
-
-// L2 eviction-priority hints.  The block stage streams the history through L2
-// (evict_first); what the latency-bound step chain reads next — the fields, the
-// newest history slices, the block's partial sums — is written evict_last so it
-// is still in L2 when read (misses would queue behind the stream in HBM).
-__device__ __forceinline__ uint64_t l2_policy_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-__device__ __forceinline__ uint64_t l2_policy_normal() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-__device__ __forceinline__ uint64_t l2_policy_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-__device__ __forceinline__ void st_pair_hint(double* p, double a, double b, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol) : "memory");
-}
-
-__device__ __forceinline__ void st_hint1(double* p, double v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-
-__device__ __forceinline__ double2 ld_cg2_hint(const double* p, uint64_t pol) {
-    double2 v;
-    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Split grid barrier.  arrive: every thread's writes of this CTA are released
-// (bar.sync + gpu-scope fence by the arriving thread); wait: acquire, then the
-// CTA proceeds.  The counter is monotonic within a launch (reset before it).
-__device__ __forceinline__ void grid_arrive(unsigned long long* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-    }
-}
-
-__device__ __forceinline__ void grid_wait(const unsigned long long* bar, unsigned long long target) {
-    if (threadIdx.x == 0) {
-        while (ld_acquire(bar) < target) __nanosleep(40);
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// ------------------------------------------------------------------- stencil ---
-// grid.py:98-105 operation order, each op correctly rounded (no contraction):
-//   2D ((((x+ + x-) - 4c) + y+) + y-); 1D (x+ + x-) - 2c; 3D with -6c, y±, z±.
-
-struct Shape {
-    int32_t n0, n1, n2;  // C-order extents (unused = 1)
-};
-
-template <int NDIM>
-__device__ __forceinline__ bool interior(const Shape& sh, int32_t q) {
-    if (NDIM == 1) return q > 0 && q < sh.n0 - 1;
-    if (NDIM == 2) {
-        const int32_t j = q / sh.n1, l = q - j * sh.n1;
-        return j > 0 && j < sh.n0 - 1 && l > 0 && l < sh.n1 - 1;
-    }
-    const int32_t plane = sh.n1 * sh.n2;
-    const int32_t i0 = q / plane, r = q - i0 * plane;
-    const int32_t i1 = r / sh.n2, i2 = r - i1 * sh.n2;
-    return i0 > 0 && i0 < sh.n0 - 1 && i1 > 0 && i1 < sh.n1 - 1 && i2 > 0 && i2 < sh.n2 - 1;
-}
-
-// Interior flags of the point pair (q, q+1) from one coordinate decomposition
-// (the per-point `interior` costs an integer division per axis).
-template <int NDIM>
-__device__ __forceinline__ void interior_pair(const Shape& sh, int32_t q, bool& in0, bool& in1) {
-    if (NDIM == 1) {
-        in0 = q > 0 && q < sh.n0 - 1;
-        in1 = q + 1 > 0 && q + 1 < sh.n0 - 1;
-    } else if (NDIM == 2) {
-        const int32_t j = q / sh.n1, l = q - j * sh.n1;
-        const bool row = j > 0 && j < sh.n0 - 1;
-        in0 = row && l > 0 && l < sh.n1 - 1;
-        // q+1 in the same row unless l is the last column (then it is a ring point)
-        in1 = row && l + 1 < sh.n1 - 1;
-    } else {
-        const int32_t plane = sh.n1 * sh.n2;
-        const int32_t i0 = q / plane, r = q - i0 * plane;
-        const int32_t i1 = r / sh.n2, i2 = r - i1 * sh.n2;
-        const bool line = i0 > 0 && i0 < sh.n0 - 1 && i1 > 0 && i1 < sh.n1 - 1;
-        in0 = line && i2 > 0 && i2 < sh.n2 - 1;
-        in1 = line && i2 + 1 < sh.n2 - 1;
-    }
-}
-
-// u is read through L2 (.cg): in the persistent kernel the field buffers are
-// rewritten every other step, so an L1 copy could be stale.
-template <int NDIM>
-__device__ __forceinline__ double delta_at(const double* __restrict__ u, const Shape& sh, int32_t q,
-                                           double c) {
-    if (!interior<NDIM>(sh, q)) return 0.0;
-    if (NDIM == 1) {
-        return __dsub_rn(__dadd_rn(ld_cg(u + q + 1), ld_cg(u + q - 1)), __dmul_rn(2.0, c));
-    } else if (NDIM == 2) {
-        const int32_t sx = sh.n1;
-        double r = __dadd_rn(ld_cg(u + q + sx), ld_cg(u + q - sx));
-        r = __dsub_rn(r, __dmul_rn(4.0, c));
-        r = __dadd_rn(r, ld_cg(u + q + 1));
-        return __dadd_rn(r, ld_cg(u + q - 1));
-    } else {
-        const int32_t sy = sh.n2, sx = sh.n1 * sh.n2;
-        double r = __dadd_rn(ld_cg(u + q + sx), ld_cg(u + q - sx));
-        r = __dsub_rn(r, __dmul_rn(6.0, c));
-        r = __dadd_rn(r, ld_cg(u + q + sy));
-        r = __dadd_rn(r, ld_cg(u + q - sy));
-        r = __dadd_rn(r, ld_cg(u + q + 1));
-        return __dadd_rn(r, ld_cg(u + q - 1));
-    }
-}
-
-// δ of the point pair (q, q+1) (q even) with every neighbour load issued before
-// any arithmetic, so the step's critical path holds one L2 round trip: the
-// other rows/planes are read as 128-bit pairs when their stride is even, the
-// outer x-neighbours u[q-1] (point q) and u[q+2] (point q+1) singly, and each
-// δ is formed in the grid.py:98-105 order exactly like delta_in.
-__device__ __forceinline__ double2 ld_pair_any(const double* p, bool even) {
-    return even ? ld_cg2(p) : make_double2(ld_cg(p), ld_cg(p + 1));
-}
-
-template <int NDIM>
-__device__ __forceinline__ void delta_pair(const double* __restrict__ u, const Shape& sh, int32_t q, double u0,
-                                           double u1, bool in0, bool in1, double& d0, double& d1) {
-    const bool any = in0 || in1;
-    const double lf = in0 ? ld_cg(u + q - 1) : 0.0;  // u[q-1] (q > 0 when in0)
-    const double rt = in1 ? ld_cg(u + q + 2) : 0.0;  // u[q+2]
-    double2 xp = make_double2(0.0, 0.0), xm = xp, yp = xp, ym = xp;
-    if (NDIM >= 2 && any) {
-        const int32_t sx = NDIM == 2 ? sh.n1 : sh.n1 * sh.n2;
-        const bool ev = (sx & 1) == 0;
-        xp = ld_pair_any(u + q + sx, ev);
-        xm = ld_pair_any(u + q - sx, ev);
-        if (NDIM == 3) {
-            const int32_t sy = sh.n2;
-            const bool evy = (sy & 1) == 0;
-            yp = ld_pair_any(u + q + sy, evy);
-            ym = ld_pair_any(u + q - sy, evy);
-        }
-    }
-    if (NDIM == 1) {
-        d0 = in0 ? __dsub_rn(__dadd_rn(u1, lf), __dmul_rn(2.0, u0)) : 0.0;
-        d1 = in1 ? __dsub_rn(__dadd_rn(rt, u0), __dmul_rn(2.0, u1)) : 0.0;
-    } else if (NDIM == 2) {
-        double r0 = __dsub_rn(__dadd_rn(xp.x, xm.x), __dmul_rn(4.0, u0));
-        r0 = __dadd_rn(__dadd_rn(r0, u1), lf);
-        double r1 = __dsub_rn(__dadd_rn(xp.y, xm.y), __dmul_rn(4.0, u1));
-        r1 = __dadd_rn(__dadd_rn(r1, rt), u0);
-        d0 = in0 ? r0 : 0.0;
-        d1 = in1 ? r1 : 0.0;
-    } else {
-        double r0 = __dsub_rn(__dadd_rn(xp.x, xm.x), __dmul_rn(6.0, u0));
-        r0 = __dadd_rn(__dadd_rn(r0, yp.x), ym.x);
-        r0 = __dadd_rn(__dadd_rn(r0, u1), lf);
-        double r1 = __dsub_rn(__dadd_rn(xp.y, xm.y), __dmul_rn(6.0, u1));
-        r1 = __dadd_rn(__dadd_rn(r1, yp.y), ym.y);
-        r1 = __dadd_rn(__dadd_rn(r1, rt), u0);
-        d0 = in0 ? r0 : 0.0;
-        d1 = in1 ? r1 : 0.0;
-    }
-}
-
-// ---------------------------------------------------------------- fused step ---
-
-struct StepArgs {
-    double* u[2];          // ping-pong fields, u^k in u[k & 1]
-    double* snap;          // single-step mode: explicit snapshot target (nullable)
-    double* pool;          // multi-step mode: snapshot pool
-    const int32_t* snap_slot;  // multi-step mode: pool slot of step `done` or -1 (nullable)
-    double* H;
-    const double* psi;
-    const double* decay;
-    const double* diffuse;
-    const double* dt;
-    const int64_t* horizon;
-    int64_t* status;
-    unsigned long long* bar;
-    int64_t k0, k1;        // steps [k0, k1)
-    int64_t slice_stride;  // B*ms
-    int64_t ms;
-    int64_t psi_stride;
-    int64_t base;
-    int64_t hz_max;        // max short-memory horizon over members
-    double vmax, km;
-    Shape sh;
-    int32_t n_m;
-    int32_t kind;
-    int32_t tpm;           // tiles per member
-    int32_t total_tiles;
-    int32_t passes;        // tiles per CTA
-    int32_t pdl_wait;      // single-step: launched as a programmatic dependent
-    int32_t pdl_trigger;   // single-step: let the next step launch early
-    int32_t m0_from_history;
-    int32_t blocked;       // temporal blocking: slices t < kb0 come from P
-    int64_t kb0;           // first step of the current block
-    const double* P;       // [tblock][B*ms] block partial sums (fg_block_kernel)
-    int64_t h_slices;      // history capacity (bounds checks)
-    int32_t tblock;        // rows of P (bounds checks)
-    int32_t recent_first;  // recent slices loaded evict_first (large fields)
-    // blocked single-step launches: the entries of step k's schedule with
-    // 2 <= m <= k-kb0 (the only ones a blocked step still sums itself), host-
-    // evaluated so the step kernel builds no schedule: offsets ascending, weights,
-    // and the weight of m = 1.  Multi-step launches build them on the device.
-    int32_t rn;
-    int32_t rw1;
-    uint8_t rm[kMaxTBlock];
-    uint8_t rwt[kMaxTBlock];
-    // single member with plan->psi_host: the coefficients themselves (w·ψ(m),
-    // rounded once on the host exactly like __dmul_rn), so the step kernel does
-    // no ψ loads and no conversions on its critical path
-    int32_t has_rc;
-    double rc0, rc1;
-    double rc[kMaxTBlock];
-};
-
-// Recent entries of step k in block kb0 (host and device): offsets 2 <= m <= bb
-// ascending with their weights, and the weight of m = 1 (0 if absent or bb = 0).
-FG_HD int recent_list(int kind, int64_t k, int64_t kb0, int64_t base, int64_t hz, uint8_t* rm, uint8_t* rwt,
-                      int32_t* w1) {
-    FgSeg segs[FG_MAX_SEGS];
-    const int64_t bb = k - kb0;
-    const int n = fg_segments(kind, k, base, hz, segs);
-    int c = 0;
-    *w1 = 0;
-    for (int i = 0; i < n; ++i) {
-        const int64_t st = segs[i].stride;
-        for (int64_t j = 0; j < segs[i].count; ++j) {
-            const int64_t m = segs[i].m0 + j * st;
-            if (m > bb) break;
-            if (m == 1) *w1 = (int32_t)st;
-            if (m >= 2) {
-                rm[c] = (uint8_t)m;
-                rwt[c] = (uint8_t)st;
-                ++c;
-            }
-        }
-    }
-    return c;
-}
-
-// Number of schedule entries with offset m <= mmax (entries ascend in m).
-__device__ __forceinline__ int64_t entries_upto(const FgSeg* s, int n, int64_t mmax) {
-    int64_t c = 0;
-    for (int i = 0; i < n; ++i) {
-        if (s[i].m0 > mmax) break;
-        const int64_t in = (mmax - s[i].m0) / s[i].stride + 1;
-        c += in < s[i].count ? in : s[i].count;
-    }
-    return c;
-}
-
-
-// General A phase (unblocked steps): schedule of step k in shared memory, every
-// entry with m >= 2 streamed into s_acc; also returns the schedule length and
-// the weight of m = 1 for phase C.  Its shared staging exists only in the
-// kernels that call it (not in the temporal-blocking variant).
-template <int S>
-__device__ __forceinline__ void general_a_phase(const StepArgs& a, int64_t k, double2* s_acc, int64_t& len,
-                                                int64_t& w1, bool& has_m1) {
-    constexpr int kCols = (kThreads / 32) / S;
-    constexpr int TP = kCols * 32 * kVec;
-    constexpr int kLanes = kCols * 32;
-    __shared__ FgSeg segs[FG_MAX_SEGS];
-    __shared__ int64_t seg_first[FG_MAX_SEGS + 1];
-    __shared__ int s_nseg;
-    __shared__ int64_t s_lim;
-    __shared__ int32_t s_t[kChunk];
-    __shared__ int32_t s_w[kChunk];
-    __shared__ double s_c[kChunk];
-    __shared__ double2 s_part[S > 1 ? (S - 1) * kLanes : 1];
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int col = warp % kCols, split = warp / kCols;
-    const int slot = col * 32 + lane;
-    const int G = gridDim.x;
-    const int64_t bb = k - a.kb0;
-    // ================= A: schedule + old slices (m >= 2) =================
-    for (int i = tid; i < a.passes * kLanes; i += kThreads) s_acc[i] = make_double2(0.0, 0.0);
-    if (tid == 0) {
-        int n = fg_segments(a.kind, k, a.base, a.hz_max, segs);
-        int64_t acc = 0;
-        for (int i = 0; i < n; ++i) {
-            seg_first[i] = acc;
-            acc += segs[i].count;
-        }
-        seg_first[n] = acc;
-        s_nseg = n;
-        // temporal blocking: entries with m > bb (slices t < kb0) are already
-        // summed into P by fg_block_kernel; only m <= bb remain for this step
-        s_lim = a.blocked ? entries_upto(segs, n, k - a.kb0) : acc;
-    }
-    __syncthreads();
-    const int nseg = s_nseg;
-    len = seg_first[nseg];
-    const int64_t lim = s_lim;
-    // entry 0 is m = 0 (every schedule opens with the dense window); entry 1 is
-    // m = 1 whenever the schedule has it.  Both depend on step k-1's output
-    // and are summed in phase C; entries from 2 on read slices t <= k-2.
-    const int64_t m1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].m0 + segs[0].stride : segs[1].m0) : 0;
-    w1 = len >= 2 ? (segs[0].count >= 2 ? segs[0].stride : segs[1].stride) : 0;
-    has_m1 = len >= 2 && m1 == 1 && (!a.blocked || bb >= 1);
-    const int64_t old = (len >= 2 && m1 == 1) ? 2 : 1;
-
-    for (int64_t c0 = old; c0 < lim; c0 += kChunk) {
-        const int cn = (int)((lim - c0) < kChunk ? (lim - c0) : kChunk);
-        for (int e = tid; e < cn; e += kThreads) {
-            const int64_t j = c0 + e;
-            int si = 0;
-            while (si + 1 < nseg && seg_first[si + 1] <= j) ++si;
-            const int64_t m = segs[si].m0 + (j - seg_first[si]) * segs[si].stride;
-            FG_DCHECK(m >= 2 && m <= k && k < a.h_slices);
-            s_t[e] = (int32_t)(k - m);
-            s_w[e] = (int32_t)segs[si].stride;
-        }
-        int64_t cur_member = -1;
-        for (int p = 0; p < a.passes; ++p) {
-            const int tile = blockIdx.x + p * G;
-            if (tile >= a.total_tiles) break;
-            const int64_t b = tile / a.tpm;
-            if (b != cur_member) {  // coefficients c = w·ψ_b(m) for this member
-                __syncthreads();
-                const double* psi_b = a.psi + b * a.psi_stride;
-                for (int e = tid; e < cn; e += kThreads)
-                    s_c[e] = __dmul_rn((double)s_w[e], __ldg(psi_b + (k - s_t[e])));
-                __syncthreads();
-                cur_member = b;
-            }
-            int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
-            if (len_b > lim) len_b = lim;
-            const int cnb = (int)(len_b <= c0 ? 0 : (len_b - c0 < cn ? len_b - c0 : cn));
-            const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
-            double acc0 = 0.0, acc1 = 0.0;
-            if (q < a.n_m) {
-                const double* hbase = a.H + b * a.ms + q;
-                for (int e0 = split; e0 < cnb; e0 += S * kUnroll) {
-                    double2 v[kUnroll];
-                    double c[kUnroll];
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u) {
-                        const int e = e0 + u * S;
-                        if (e < cnb) {
-                            v[u] = ld_stream(hbase + (int64_t)s_t[e] * a.slice_stride);
-                            c[u] = s_c[e];
-                        } else {
-                            v[u] = make_double2(0.0, 0.0);
-                            c[u] = 0.0;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u) {
-                        acc0 = fma(c[u], v[u].x, acc0);
-                        acc1 = fma(c[u], v[u].y, acc1);
-                    }
-                }
-            }
-            if (S > 1) {
-                if (split > 0) s_part[(split - 1) * kLanes + slot] = make_double2(acc0, acc1);
-                __syncthreads();
-                if (split == 0) {
-#pragma unroll
-                    for (int s = 1; s < S; ++s) {
-                        const double2 pp = s_part[(s - 1) * kLanes + slot];
-                        acc0 = __dadd_rn(acc0, pp.x);
-                        acc1 = __dadd_rn(acc1, pp.y);
-                    }
-                }
-                __syncthreads();
-            }
-            if (split == 0) {
-                double2& r = s_acc[p * kLanes + slot];
-                r.x = __dadd_rn(r.x, acc0);
-                r.y = __dadd_rn(r.y, acc1);
-            }
-        }
-        __syncthreads();  // s_t / s_w / s_c are refilled by the next chunk
-    }
-}
-
-// BLK: temporal-blocking variant (S = 1): the recent-slice A phase only, no
-// shared staging, so two of its CTAs fit next to two block-kernel CTAs per SM.
-template <int NDIM, int REACT, int S, bool BLK>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) fg_step_kernel(const __grid_constant__ StepArgs a) {
-    constexpr int kCols = (kThreads / 32) / S;   // warps across a tile
-    constexpr int TP = kCols * 32 * kVec;        // points per tile
-    constexpr int kLanes = kCols * 32;           // split-0 threads (one point pair each)
-    extern __shared__ double2 s_acc[];  // [passes][kLanes] partial sums of the A phase
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int col = warp % kCols, split = warp / kCols;
-    const int slot = col * 32 + lane;
-    const int G = gridDim.x;
-    const bool multi = a.k1 - a.k0 > 1;
-
-    for (int64_t k = a.k0; k < a.k1; ++k) {
-        const int64_t bb = k - a.kb0;
-        int64_t len, w1;   // schedule length (kinds 0/2), weight of m = 1
-        bool has_m1;
-        if constexpr (BLK) {
-            // ====== A (temporal blocking): recent slices 2 <= m <= bb only ======
-            // Everything older is in P[bb].  Single-step launches get the recent
-            // entries from the host (no schedule, no shared staging, no CTA
-            // barrier); multi-step launches build them here.  Same entry order
-            // and rounding as the general path.
-            __shared__ uint8_t s_rm[kMaxTBlock], s_rwt[kMaxTBlock];
-            __shared__ int32_t s_rn, s_w1;
-            const uint8_t* rm = a.rm;
-            const uint8_t* rwt = a.rwt;
-            const double* rcoef = a.has_rc ? a.rc : nullptr;
-            int rn = a.rn;
-            w1 = a.rw1;
-            if (multi) {
-                if (tid == 0) s_rn = recent_list(a.kind, k, a.kb0, a.base, a.hz_max, s_rm, s_rwt, &s_w1);
-                __syncthreads();
-                rm = s_rm;
-                rwt = s_rwt;
-                rcoef = nullptr;
-                rn = s_rn;
-                w1 = s_w1;
-            }
-            has_m1 = w1 != 0;
-#ifdef FG_DBG_NO_RECENT  // timing experiment only: drop the recent sum (wrong results)
-            rn = 0;
-#endif
-            len = k + 1;  // only used for the m = 1 test below (k >= bb >= 1)
-            for (int p = 0; p < a.passes; ++p) {
-                const int tile = blockIdx.x + p * G;
-                if (tile >= a.total_tiles) break;
-                const int64_t b = tile / a.tpm;
-                const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
-                double acc0 = 0.0, acc1 = 0.0;
-                // P[bb] (slices t < kb0) is final before the block's first step
-                // starts: its load is issued first and added after the recent sum,
-                // all before the dependency wait (same order as the unblocked path)
-                const double2 pb = q < a.n_m ? ld_cg2_hint(a.P + bb * a.slice_stride + b * a.ms + q, l2_policy_first())
-                                             : make_double2(0.0, 0.0);  // its only read
-                FG_DCHECK(bb >= 0 && bb < a.tblock && k < a.h_slices && rn <= bb);
-                if (q < a.n_m && rn > 0) {
-                    const uint64_t pol_drop = a.recent_first ? l2_policy_first() : l2_policy_normal();
-                    const double* hbase = a.H + b * a.ms + q + k * a.slice_stride;
-                    const double* psi_b = a.psi + b * a.psi_stride;
-                    const int64_t mmax = a.kind == 1 ? (a.horizon[b] < bb ? a.horizon[b] : bb) : bb;
-#ifndef FG_STEP_KR
-#define FG_STEP_KR 5
-#endif
-                    constexpr int kR = REACT ? FG_STEP_KR - 1 : FG_STEP_KR;  // recent slices in flight per round (no spills)
-#pragma unroll 1
-                    // entries oldest first (descending m): the fused pair kernel must
-                    // add the newest ones after its dependency wait, in the same order
-                    for (int e0 = 0; e0 < rn; e0 += kR) {
-                        double2 v[kR];
-                        double c[kR];
-#pragma unroll
-                        for (int u = 0; u < kR; ++u) {
-                            const int e = rn - 1 - (e0 + u);
-                            const int m = e >= 0 ? rm[e] : 0;
-                            const bool on = e >= 0 && m <= mmax;
-                            FG_DCHECK(!on || (m >= 2 && m <= k));
-                            if (on) {
-                                // large fields: evict_first — keeping even the newest slices in
-                                // L2 (offsets <= 3, 5 or 9 evict_last) measured slower than
-                                // streaming them (c4-adaptive 589 vs 599-610 ms); small fields'
-                                // recent slices stay in L2 (c2)
-                                v[u] = ld_cg2_hint(hbase - (int64_t)m * a.slice_stride, pol_drop);
-                                c[u] = rcoef ? rcoef[e] : __dmul_rn((double)rwt[e], __ldg(psi_b + m));
-                            } else {
-                                v[u] = make_double2(0.0, 0.0);
-                                c[u] = 0.0;
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < kR; ++u) {
-                            acc0 = fma(c[u], v[u].x, acc0);
-                            acc1 = fma(c[u], v[u].y, acc1);
-                        }
-                    }
-                }
-                s_acc[p * kLanes + slot] =
-                    make_double2(__dadd_rn(__dadd_rn(0.0, acc0), pb.x), __dadd_rn(__dadd_rn(0.0, acc1), pb.y));
-            }
-        } else {
-            general_a_phase<S>(a, k, s_acc, len, w1, has_m1);
-        }
-
-        // ================= dependency on step k-1 =================
-        if (multi) {
-            if (k > a.k0) grid_wait(a.bar, (unsigned long long)(k - a.k0) * (unsigned long long)G);
-        } else {
-            if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
-            // step k-1 is complete, so every slice t <= k-1 is final: let step k+1
-            // start its A phase in the slots this grid frees
-            if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;");
-        }
-        // u^j non-finite for some j <= k: this step must not run.  The flag is
-        // loaded now but tested only before the stores, so its L2 round trip
-        // overlaps the C-phase loads.  A flag for step k+1 raised during this
-        // step's C phase by another CTA is ignored, so every CTA leaves at the
-        // same step (no CTA can strand the others at the barrier).
-        const bool live = *(volatile const int64_t*)a.status > k;
-
-        // ================= C: m = 1, m = 0, update =================
-        const uint64_t keep = l2_policy_last(), drop = l2_policy_first();
-        const double* u_in = a.u[k & 1];
-        double* u_out = a.u[(k + 1) & 1];
-        double* snap = a.snap;
-        if (a.snap_slot) {  // persistent launches: snapshot slot of step k+1 from the map
-            const int32_t sl = a.snap_slot[k + 1];
-            snap = sl >= 0 ? a.pool + (int64_t)sl * a.slice_stride : nullptr;
-        }
-        if (split == 0) {
-            for (int p = 0; p < a.passes; ++p) {
-                const int tile = blockIdx.x + p * G;
-                if (tile >= a.total_tiles) break;
-                const int64_t b = tile / a.tpm;
-                const int32_t q = (tile % a.tpm) * TP + col * 64 + lane * kVec;
-                if (q >= a.n_m) continue;
-                const int64_t moff = b * a.ms + q;
-                const double* ub = u_in + b * a.ms;
-                const double* psi_b = a.psi + b * a.psi_stride;
-                FG_DCHECK(k < a.h_slices && k < a.psi_stride && q + 1 < a.ms + 1 && b < a.slice_stride / a.ms);
-                // every load of the C phase is issued before any arithmetic or
-                // store (one L2 round trip on the step chain's critical path)
-                const int64_t len_b = a.kind == 1 ? ((a.horizon[b] < k ? a.horizon[b] : k) + 1) : len;
-                const bool m1 = has_m1 && len_b >= 2;
-                const double2 h1 = m1 ? ld_cg2(a.H + (k - 1) * a.slice_stride + moff) : make_double2(0.0, 0.0);
-                const double2 pb = (!BLK && a.blocked) ? ld_cg2_hint(a.P + bb * a.slice_stride + moff, drop)
-                                                       : make_double2(0.0, 0.0);
-                const double2 uu = ld_cg2(ub + q);
-                const double u0 = uu.x, u1 = uu.y;
-                bool in0, in1;
-                interior_pair<NDIM>(a.sh, q, in0, in1);
-                in1 = in1 && q + 1 < a.n_m;
-                double d0, d1;
-                if (a.m0_from_history) {
-                    const double2 h = ld_cg2(a.H + k * a.slice_stride + moff);
-                    d0 = h.x;
-                    d1 = h.y;
-                } else {
-                    delta_pair<NDIM>(ub, a.sh, q, u0, u1, in0, in1, d0, d1);
-                }
-                const double2 part = s_acc[p * kLanes + slot];
-                double acc0 = part.x, acc1 = part.y;
-                if (!BLK && a.blocked) {  // slices t < kb0 (the BLK kernel added them before the wait)
-                    acc0 = __dadd_rn(acc0, pb.x);
-                    acc1 = __dadd_rn(acc1, pb.y);
-                }
-                const bool host_c = BLK && a.has_rc && !multi;  // single-member coefficients, precomputed
-                if (m1) {
-                    const double c1 = host_c ? a.rc1 : __dmul_rn((double)w1, __ldg(psi_b + 1));
-                    acc0 = fma(c1, h1.x, acc0);
-                    acc1 = fma(c1, h1.y, acc1);
-                }
-                const double c0 = host_c ? a.rc0 : __ldg(psi_b);  // w_0 * ψ(0) = 1 * 1
-                acc0 = fma(c0, d0, acc0);
-                acc1 = fma(c0, d1, acc1);
-
-                // solver.py:215-226 rounding order, ring pinned, non-finite check
-                const double diffuse = a.diffuse[b];
-                double n0, n1;
-                if (REACT == 0) {
-                    const double decay = a.decay[b];
-                    n0 = __dadd_rn(__dmul_rn(u0, decay), __dmul_rn(diffuse, acc0));
-                    n1 = __dadd_rn(__dmul_rn(u1, decay), __dmul_rn(diffuse, acc1));
-                } else {
-                    const double dt = a.dt[b];
-                    const double f0 = __ddiv_rn(__dmul_rn(-a.vmax, u0), __dadd_rn(a.km, u0));
-                    const double f1 = __ddiv_rn(__dmul_rn(-a.vmax, u1), __dadd_rn(a.km, u1));
-                    n0 = __dadd_rn(__dadd_rn(u0, __dmul_rn(dt, f0)), __dmul_rn(diffuse, acc0));
-                    n1 = __dadd_rn(__dadd_rn(u1, __dmul_rn(dt, f1)), __dmul_rn(diffuse, acc1));
-                }
-                if (!in0) n0 = 0.0;
-                if (!in1) n1 = 0.0;
-                if (!live) break;
-                if (!a.m0_from_history) st_pair_hint(a.H + k * a.slice_stride + moff, d0, d1, keep);
-                if (!isfinite(n0) || !isfinite(n1))
-                    atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
-                st_pair_hint(u_out + moff, n0, n1, keep);
-                if (snap) st_pair_hint(snap + moff, n0, n1, drop);
-            }
-        }
-        if (!live) return;  // uniform: every thread read the same flag
-        if (multi) grid_arrive(a.bar);
-    }
-}
-
-// ------------------------------------------------------- fused step pairs ---
-// Steps k and k+1 of a temporal block in one launch (1D and 2D fields): a CTA
-// computes step k on its tile plus a halo of R points each side (R = 1 in 1D,
-// one row in 2D) from u^k staged in shared memory, then step k+1 on its tile
-// from those values, so the step chain pays one kernel boundary and one L2
-// round trip per two steps.  The halo points' values are recomputed with the
-// very same arithmetic as by their owning CTA (bit-identical results).
-// Before the dependency wait only slices written two launches back are read:
-// step k's recent entries with m >= 3 and step k+1's with m >= 4 (oldest
-// first, the order the single-step kernel uses); m = 2 (step k) and m = 3, 2
-// (step k+1) and the m = 1 terms are added after it.
-// u buffers: the pair reads u^k from `u_in`, writes u^{k+1} of its tile to the
-// parity buffer u[(k+1) & 1] (the divergence report reads it) and u^{k+2} to
-// `u_out`, which no CTA of the launch reads: pairs alternate between a library
-// scratch buffer and the parity buffer u[k & 1], and run in even numbers so the
-// field is back in its parity buffer after each sequence.  *u3_step records
-// which step's field sits in the scratch buffer (fg_u3_fixup_kernel).
-// Recent list of one blocked step (the pair kernel's second step).
-struct RecentRow {
-    int32_t rn, rw1;
-    double rc0, rc1;
-    uint8_t rm[kMaxTBlock];
-    uint8_t rwt[kMaxTBlock];
-    double rc[kMaxTBlock];
-};
-
-struct PairArgs {
-    StepArgs s;                // step k: shared fields, recent list, P (block kb0)
-    RecentRow r2;              // step k+1's recent list
-    const double* u_in;        // u^k
-    double* u_mid;             // u^{k+1} (own tile) = u[(k+1) & 1]
-    double* u_out;             // u^{k+2}
-    double* snap1;             // snapshot of u^{k+1} (or NULL)
-    double* snap2;             // snapshot of u^{k+2} (or NULL)
-    int64_t* u3_step;
-    int32_t writes_u3;
-};
-constexpr int kPairTile = 512;                 // points per CTA (as the blocked step kernel)
-constexpr int kPairMaxHalo = 256;              // R <= 256
-constexpr int kPairNP = (kPairTile + 2 * kPairMaxHalo + kThreads - 1) / kThreads;  // extended points per thread
-
-template <int NDIM, int REACT>
-__global__ void __launch_bounds__(kThreads, 2) fg_step2_kernel(const __grid_constant__ PairArgs A) {
-    const StepArgs& a = A.s;
-    extern __shared__ double sm2[];
-    const int tid = threadIdx.x;
-    const int tile = blockIdx.x;
-    const int64_t b = tile / a.tpm;
-    const int32_t q0 = (tile % a.tpm) * kPairTile;
-    const int32_t n = a.n_m;
-    const int32_t R = NDIM == 1 ? 1 : a.sh.n1;
-    const int32_t o_lo = q0, o_hi = q0 + kPairTile < n ? q0 + kPairTile : n;
-    const int32_t lo = o_lo - R > 0 ? o_lo - R : 0, hi = o_hi + R < n ? o_hi + R : n;    // extended range E
-    const int32_t ulo = lo - R > 0 ? lo - R : 0, uhi = hi + R < n ? hi + R : n;          // u^k staged
-    double* su = sm2;                                  // [uhi - ulo] u^k
-    double* su1 = sm2 + (kPairTile + 4 * kPairMaxHalo);  // [hi - lo]  u^{k+1}
-    const int64_t k = a.k0, bb = k - a.kb0;
-    const int64_t ss = a.slice_stride;
-    const double* Hm = a.H + b * a.ms;                 // member's slice rows
-    const double* psi_b = a.psi + b * a.psi_stride;
-    const bool hc = a.has_rc != 0;
-    const RecentRow& r2 = A.r2;
-    auto coef1 = [&](int e) { return hc ? a.rc[e] : __dmul_rn((double)a.rwt[e], __ldg(psi_b + a.rm[e])); };
-    auto coef2 = [&](int e) { return hc ? r2.rc[e] : __dmul_rn((double)r2.rwt[e], __ldg(psi_b + r2.rm[e])); };
-
-    // ---- A (before the dependency): P rows and the recent entries two launches old
-    double acc1[kPairNP], acc2[kPairNP], pb1[kPairNP], pb2[kPairNP];
-#pragma unroll
-    for (int j = 0; j < kPairNP; ++j) {
-        const int32_t p = lo + tid + j * kThreads;
-        acc1[j] = acc2[j] = pb1[j] = pb2[j] = 0.0;
-        if (p < hi) pb1[j] = ld_cg(a.P + bb * ss + b * a.ms + p);
-        if (p >= o_lo && p < o_hi) pb2[j] = ld_cg(a.P + (bb + 1) * ss + b * a.ms + p);
-    }
-    // rounds of kPR entries x kPairNP points in flight (oldest first); padding
-    // entries add fma(0, 0, acc), which leaves every nonzero partial unchanged
-    // and is normalised away by the __dadd_rn(0, .) below, as in the step kernel
-    constexpr int kPR = 3;
-    {
-        int n1 = 0;  // step k: entries m >= 3 are the last n1 of the list
-        while (n1 < a.rn && a.rm[a.rn - 1 - n1] >= 3) ++n1;
-        for (int e0 = 0; e0 < n1; e0 += kPR) {
-            double v[kPR][kPairNP], c[kPR];
-#pragma unroll
-            for (int u = 0; u < kPR; ++u) {
-                const int e = a.rn - 1 - (e0 + u);
-                const bool on = e0 + u < n1;
-                c[u] = on ? coef1(e) : 0.0;
-                const double* h = Hm + (k - (on ? a.rm[e] : 0)) * ss;
-#pragma unroll
-                for (int j = 0; j < kPairNP; ++j) {
-                    const int32_t p = lo + tid + j * kThreads;
-                    v[u][j] = (on && p < hi) ? ld_cg(h + p) : 0.0;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kPR; ++u)
-#pragma unroll
-                for (int j = 0; j < kPairNP; ++j) acc1[j] = fma(c[u], v[u][j], acc1[j]);
-        }
-        int n2 = 0;  // step k+1: entries m >= 4
-        while (n2 < r2.rn && r2.rm[r2.rn - 1 - n2] >= 4) ++n2;
-        for (int e0 = 0; e0 < n2; e0 += kPR) {
-            double v[kPR][kPairNP / 2], c[kPR];
-#pragma unroll
-            for (int u = 0; u < kPR; ++u) {
-                const int e = r2.rn - 1 - (e0 + u);
-                const bool on = e0 + u < n2;
-                c[u] = on ? coef2(e) : 0.0;
-                const double* h = Hm + (k + 1 - (on ? r2.rm[e] : 0)) * ss;
-#pragma unroll
-                for (int j = 0; j < kPairNP; ++j) {
-                    const int32_t p = lo + tid + j * kThreads;
-                    const bool own = p >= o_lo && p < o_hi;
-                    if (j < kPairNP / 2) v[u][j] = 0.0;
-                    if (own) v[u][j % (kPairNP / 2)] = on ? ld_cg(h + p) : 0.0;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kPR; ++u)
-#pragma unroll
-                for (int j = 0; j < kPairNP; ++j) {
-                    const int32_t p = lo + tid + j * kThreads;
-                    if (p >= o_lo && p < o_hi) acc2[j] = fma(c[u], v[u][j % (kPairNP / 2)], acc2[j]);
-                }
-        }
-    }
-
-    // ---- dependency on the previous launch (steps k-2, k-1)
-    if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;");
-    const bool live = *(volatile const int64_t*)a.status > k;
-
-    // ---- C: stage u^k, then the newest history terms
-    const double* ub = A.u_in + b * a.ms;
-    for (int32_t i = tid; i < uhi - ulo; i += kThreads) su[i] = ld_cg(ub + ulo + i);
-    double h1[kPairNP], h2[kPairNP];
-#pragma unroll
-    for (int j = 0; j < kPairNP; ++j) {
-        const int32_t p = lo + tid + j * kThreads;
-        h1[j] = h2[j] = 0.0;
-        if (p < hi) {
-            if (k >= 1) h1[j] = ld_cg(Hm + (k - 1) * ss + p);
-            if (k >= 2) h2[j] = ld_cg(Hm + (k - 2) * ss + p);
-        }
-    }
-    __syncthreads();
-    // entries m = 3 / 2 of a list (ascending, so they are the first ones)
-    int e1_2 = -1, e2_2 = -1, e2_3 = -1;
-    for (int e = 0; e < a.rn && a.rm[e] <= 3; ++e)
-        if (a.rm[e] == 2) e1_2 = e;
-    for (int e = 0; e < r2.rn && r2.rm[e] <= 3; ++e) {
-        if (r2.rm[e] == 2) e2_2 = e;
-        if (r2.rm[e] == 3) e2_3 = e;
-    }
-    const int64_t len_k = k + 1;  // kinds full/adaptive (short memory never pairs)
-    const double decay = a.decay[b], diffuse = a.diffuse[b];
-    double d1[kPairNP], u1[kPairNP];
-    // step k on E
-#pragma unroll
-    for (int j = 0; j < kPairNP; ++j) {
-        const int32_t p = lo + tid + j * kThreads;
-        d1[j] = u1[j] = 0.0;
-        if (p >= hi) continue;
-        double acc = acc1[j];
-        if (e1_2 >= 0) acc = fma(coef1(e1_2), h2[j], acc);
-        acc = __dadd_rn(__dadd_rn(0.0, acc), pb1[j]);
-        if (a.rw1 != 0 && len_k >= 2) acc = fma(hc ? a.rc1 : __dmul_rn((double)a.rw1, __ldg(psi_b + 1)), h1[j], acc);
-        const bool in = interior<NDIM>(a.sh, p);
-        const double c = su[p - ulo];
-        double d = 0.0;
-        if (in) {
-            if (NDIM == 1) {
-                d = __dsub_rn(__dadd_rn(su[p + 1 - ulo], su[p - 1 - ulo]), __dmul_rn(2.0, c));
-            } else {
-                double r = __dadd_rn(su[p + R - ulo], su[p - R - ulo]);
-                r = __dsub_rn(r, __dmul_rn(4.0, c));
-                r = __dadd_rn(r, su[p + 1 - ulo]);
-                d = __dadd_rn(r, su[p - 1 - ulo]);
-            }
-        }
-        acc = fma(hc ? a.rc0 : __ldg(psi_b), d, acc);
-        double nu;
-        if (REACT == 0) {
-            nu = __dadd_rn(__dmul_rn(c, decay), __dmul_rn(diffuse, acc));
-        } else {
-            const double f = __ddiv_rn(__dmul_rn(-a.vmax, c), __dadd_rn(a.km, c));
-            nu = __dadd_rn(__dadd_rn(c, __dmul_rn(a.dt[b], f)), __dmul_rn(diffuse, acc));
-        }
-        if (!in) nu = 0.0;
-        d1[j] = d;
-        u1[j] = nu;
-        su1[p - lo] = nu;
-    }
-    __syncthreads();
-    if (!live) return;
-    const uint64_t keep = l2_policy_last(), drop = l2_policy_first();
-    const int64_t moff = b * a.ms;
-    // step k+1 on the tile
-#pragma unroll
-    for (int j = 0; j < kPairNP; ++j) {
-        const int32_t p = lo + tid + j * kThreads;
-        if (p < o_lo || p >= o_hi) continue;
-        double acc = acc2[j];
-        if (e2_3 >= 0) acc = fma(coef2(e2_3), h2[j], acc);
-        if (e2_2 >= 0) acc = fma(coef2(e2_2), h1[j], acc);
-        acc = __dadd_rn(__dadd_rn(0.0, acc), pb2[j]);
-        if (r2.rw1 != 0) acc = fma(hc ? r2.rc1 : __dmul_rn((double)r2.rw1, __ldg(psi_b + 1)), d1[j], acc);
-        const bool in = interior<NDIM>(a.sh, p);
-        const double c = u1[j];
-        double d = 0.0;
-        if (in) {
-            if (NDIM == 1) {
-                d = __dsub_rn(__dadd_rn(su1[p + 1 - lo], su1[p - 1 - lo]), __dmul_rn(2.0, c));
-            } else {
-                double r = __dadd_rn(su1[p + R - lo], su1[p - R - lo]);
-                r = __dsub_rn(r, __dmul_rn(4.0, c));
-                r = __dadd_rn(r, su1[p + 1 - lo]);
-                d = __dadd_rn(r, su1[p - 1 - lo]);
-            }
-        }
-        acc = fma(hc ? r2.rc0 : __ldg(psi_b), d, acc);
-        double nu;
-        if (REACT == 0) {
-            nu = __dadd_rn(__dmul_rn(c, decay), __dmul_rn(diffuse, acc));
-        } else {
-            const double f = __ddiv_rn(__dmul_rn(-a.vmax, c), __dadd_rn(a.km, c));
-            nu = __dadd_rn(__dadd_rn(c, __dmul_rn(a.dt[b], f)), __dmul_rn(diffuse, acc));
-        }
-        if (!in) nu = 0.0;
-        if (!isfinite(u1[j])) atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 1));
-        if (!isfinite(nu)) atomicMin(reinterpret_cast<long long*>(a.status), (long long)(k + 2));
-        st_hint1(a.H + k * ss + moff + p, d1[j], keep);
-        st_hint1(a.H + (k + 1) * ss + moff + p, d, keep);
-        st_hint1(A.u_mid + moff + p, u1[j], keep);
-        st_hint1(A.u_out + moff + p, nu, keep);
-        if (A.snap1) st_hint1(A.snap1 + moff + p, u1[j], drop);
-        if (A.snap2) st_hint1(A.snap2 + moff + p, nu, drop);
-    }
-    if (tile == 0 && tid == 0) *A.u3_step = A.writes_u3 ? k + 2 : -1;
-}
-
-// After a run with pair launches: when the run stopped at a step whose field
-// sits in the scratch buffer, copy it to its parity buffer (the divergence
-// report and the caller read u[step & 1]).
-__global__ void fg_u3_fixup_kernel(const int64_t* status, const int64_t* u3_step, const double* u3, double* u0,
-                                   double* u1, int64_t n) {
-    const int64_t s = *u3_step;
-    if (s < 0 || *status != s) return;
-    double* dst = (s & 1) ? u1 : u0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = u3[i];
-}
-
-// ------------------------------------------------------- temporal blocking ---
-// fg_block_tma_kernel: one pass over the history slices t < kb0 feeds the old
-// part of the next `bt` steps (kb0 .. kb0+bt-1) at once:
-//     P[b][p] = Σ_{t < kb0} c_b(t)·H[t][p],  c_b(t) = w·ψ(kb0+b-t) if
-//               kb0+b-t is in the schedule of step kb0+b (weight w), else 0,
-// so each slice of the union of the bt schedules is read from HBM once instead of
-// once per step that visits it (full/short memory: bt× fewer bytes; adaptive:
-// the thinned intervals' strides < bt share slices).  The step kernel then adds
-// P[b] and only its recent entries (m <= b).
-
-constexpr int kBlkSegs = 32;     // segments kept per step (host checks the bound)
-
-struct BlockArgs {
-    const double* H;
-    double* P;
-    const double* psi;
-    const int64_t* horizon;
-    int64_t slice_stride, ms, psi_stride, base;
-    int64_t kb0;
-    int64_t t_begin, t_end;  // slices summed by this launch: [t_begin, t_end) ∩ [t_lo, kb0)
-    int32_t bt;
-    int32_t n_m, kind, tpm, total_tiles;
-    int32_t accumulate;      // P += D (tail launch) instead of P = D
-    const double* gcoef;  // precomputed coefficient rows (or NULL): single member, or
-                          // itemized ensembles ([B][coef_mstride] per block buffer)
-    int64_t coef_mstride; // doubles between members' coefficient rows (ensembles)
-    int64_t h_alloc;      // slices allocated at H (bounds checks)
-    int32_t tblock;       // rows of the P buffer (bounds checks)
-};
-
-// The history rows are moved by the bulk-copy engine (cp.async.bulk → shared
-// memory, mbarrier complete_tx): one producer warp keeps kStages × kE slice rows
-// in flight per CTA independent of registers; TP/32 consumer warps turn each
-// stage into DMMA m8n8k4 tiles (below).  Candidate slices are all t in
-// [t_lo, kb0) (the union covers nearly all of them: full/short memory exactly,
-// adaptive whenever the thinned strides are < BT); slices no step uses get zero
-// coefficients, exactly like the reference's zero-weighted terms.  The
-// coefficient table for the next kCH slices is built by the consumers while the
-// producer's copies for those slices are already in flight.
-
-constexpr int kE = 8;        // slice rows per stage
-constexpr int kCH = 128;     // slices per coefficient table (multiple of kE)
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-
-// Release a ring slot only once the warp's tensor-core work on it has consumed
-// its shared-memory operands: the fake `dep` input (a result of the warp's last
-// DMMA) makes the arrive wait for that DMMA, hence for every LDS feeding the
-// warp-wide DMMAs before it.  Without it ptxas scheduled the arrive right after
-// the LDS *issue*, letting the producer's next bulk copy overwrite rows still
-// being read (a rare, TP-dependent race).
-__device__ __forceinline__ void mbar_arrive_after(uint64_t* b, double dep, double* sink) {
-    asm volatile(
-        "st.shared.f64 [%2], %1;\n\t"
-        "mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)),
-        "d"(dep), "r"(smem_u32(sink))
-        : "memory");
-}
-
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-
-// History rows are streamed once per block: mark them evict-first in L2 so the
-// stream does not push out what the concurrently running steps touch (fields,
-// partial sums, the recent slices), which would turn their L2 hits into HBM
-// misses queued behind the stream.
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// Padded shared-memory rows: +4 doubles (32 B) per row puts the 4 k-rows a DMMA
-// B-fragment load touches in disjoint bank quarters (conflict-free LDS.64).
-template <int TP>
-__host__ __device__ constexpr int row_pitch() { return TP + 4; }
-template <int BT>
-__host__ __device__ constexpr int coef_pitch() { return BT + 4; }
-
-#ifndef FG_STAGED_RING
-#define FG_STAGED_RING 6
-#endif
-template <bool STAGED>
-__host__ __device__ constexpr int ring_stages() { return STAGED ? FG_STAGED_RING : 4; }
-
-constexpr int kMainStages = FG_STAGED_RING;  // staged main launches
-#ifndef FG_TAIL_STAGES
-#define FG_TAIL_STAGES 2
-#endif
-constexpr int kTailStages = FG_TAIL_STAGES;  // tail launches: small ring, so they fit beside two main CTAs per SM
-
-// slice rows per stage of the dense kernel: 16 for the 4-M-tile blocks (lean
-// consumers), kE otherwise; rings keep their bytes (fewer, deeper stages)
-template <int BT>
-__host__ __device__ constexpr int dense_ke() { return BT / 8 == 4 ? 16 : kE; }
-
-template <int BT, int TP, bool STAGED, int NS, int WP>
-size_t tma_block_smem() {
-    constexpr int KE = dense_ke<BT>();
-    constexpr int CROWS = STAGED ? NS * KE : kCH;
-    return (size_t)NS * KE * row_pitch<TP>() * sizeof(double) + (size_t)CROWS * coef_pitch<BT>() * sizeof(double) +
-           (2 * NS) * sizeof(uint64_t) + (TP / WP) * sizeof(double) +
-           (STAGED ? 0 : (size_t)BT * kBlkSegs * sizeof(FgSeg) + BT * sizeof(int));
-}
-
-// Item flushes add into P with reductions performed at L2 (no load round trip
-// in the consumer warps).  Still deterministic: a step's row is touched by one
-// lane per item, and the __syncwarp before every flush orders the previous
-// item's store/adds (other lanes) before this one's, so the adds reach each
-// element in table order — the same rounding as the load-add-store they replace.
-__device__ __forceinline__ void red_add(double* p, double v) {
-    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
-
-// Coefficient rows of a block, one per candidate slice t (pitch CP doubles):
-// row[t - t_lo][b] = w·ψ(kb0+b-t) if kb0+b-t is in the schedule of step kb0+b.
-// Single-member runs compute them once per block (all CTAs of the block kernel
-// then bulk-copy their rows next to the history rows): the rows are zeroed
-// (cudaMemsetAsync) and CTA b scatters its step's entries with t < kb0 by
-// walking the schedule segments — no per-slice search, no 64-bit divisions.
-template <int BT>
-__global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out) {
-    constexpr int CP = coef_pitch<BT>();
-    __shared__ FgSeg segs[FG_MAX_SEGS];
-    __shared__ int nseg;
-    const int bb = blockIdx.x;
-    const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
-    const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
-    const int64_t ts = a.t_begin > t_lo ? a.t_begin : t_lo, te = a.t_end;  // rows t - ts, t in [ts, te)
-    const int64_t k = a.kb0 + bb;
-    if (threadIdx.x == 0) nseg = fg_segments(a.kind, k, a.base, hz, segs);
-    __syncthreads();
-    for (int si = 0; si < nseg; ++si) {
-        // entries m = m0 + i*stride with t = k - m in [ts, te)
-        const int64_t m0 = segs[si].m0, st = segs[si].stride, cnt = segs[si].count;
-        const int64_t m_min = k - te + 1, m_max = k - ts;
-        if (m_max < m0 || m_min > m0 + (cnt - 1) * st) continue;
-        const int64_t i0 = m_min > m0 ? (m_min - m0 + st - 1) / st : 0;
-        const int64_t i1 = (m_max - m0) / st < cnt - 1 ? (m_max - m0) / st : cnt - 1;
-        for (int64_t i = i0 + threadIdx.x; i <= i1; i += blockDim.x) {
-            const int64_t m = m0 + i * st;
-            FG_DCHECK(k - m >= ts && k - m < te && ((k - m - ts) + 1) * CP <= a.coef_mstride && m < a.psi_stride);
-            out[(k - m - ts) * CP + bb] = __dmul_rn((double)st, __ldg(a.psi + m));
-        }
-    }
-}
-
-// The block's old-part sums are a small GEMM per tile: P[BT x TP] += C[BT x 8] ·
-// R[8 x TP] per stage (C = coefficients of 8 slices, R = their rows).  Consumers
-// feed it to the fp64 tensor pipe (DMMA m8n8k4: 256 FMAs per warp instruction,
-// fragments loaded straight from shared memory) instead of 16 FMAs + 9 shared
-// loads per element, which made the scalar version shared-memory-issue bound.
-// Coefficients: single member → precomputed rows (fg_block_coef_kernel) copied
-// into the ring with each stage; ensembles (per-member ψ) → a kCH-slice table
-// rebuilt by the consumers at chunk boundaries (scatter over segments).
-// WP: points per consumer warp (NT = WP/8 DMMA N tiles).  32-point warps share
-// each A fragment over 4 N tiles; 16-point warps hold half the accumulators, so
-// a CTA can have twice the warps (measured: the fp64 tensor pipe reaches its
-// peak only with 4 issuing warps per SM sub-partition, 16 per SM —
-// scripts/micro/dense_consumer.cu; 7-warp CTAs stop at 7/8 of it).
-template <int BT, int TP, bool STAGED, int NS, int WP>
-__global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
-    constexpr int kStages = NS;
-    constexpr int KE = dense_ke<BT>();  // slice rows per stage
-    static_assert(KE < 32, "one producer lane per stage row, lane 31 copies the coefficient rows");
-    constexpr int RP = row_pitch<TP>();
-    constexpr int CP = coef_pitch<BT>();
-    constexpr int MT = BT / 8;  // M tiles (steps)
-    constexpr int NT = WP / 8;  // N tiles of 8 points per warp
-    constexpr int NW = TP / WP; // consumer warps
-    constexpr int NC = NW * 32; // consumer threads
-    // lean fragments (see the stage loop) for the 4-M-tile blocks: 96 instead of
-    // ~125 registers, so 8-warp CTAs (TP 256) fit two per SM
-    constexpr bool LEAN = MT == 4;
-    constexpr int CROWS = STAGED ? kStages * KE : kCH;
-    extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);                  // [kStages][KE][RP]
-    double* coef = rows + kStages * KE * RP;                        // [CROWS][CP]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + CROWS * CP);  // [kStages]
-    uint64_t* empty = full + kStages;                               // [kStages]
-    double* sink = reinterpret_cast<double*>(empty + kStages);      // [NW] release dependencies
-    FgSeg* segs = reinterpret_cast<FgSeg*>(sink + NW);              // [BT][kBlkSegs]
-    int* nseg = reinterpret_cast<int*>(segs + BT * kBlkSegs);       // [BT]
-    constexpr bool staged = STAGED;  // coefficient rows travel with the stage (single member)
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    // Tiles blockIdx.x, +gridDim.x, ...: single-member launches run one CTA per
-    // SM over several tiles (room for the concurrent step kernel); ensembles
-    // launch one CTA per tile, so every tile of a CTA has the same member.
-    const int64_t mem = blockIdx.x / a.tpm;
-    const int64_t hz = a.kind == 1 ? a.horizon[mem] : 0;
-    // oldest slice any step of the block can reach: short memory stops at kb0 - H
-    const int64_t t_lo = (a.kind == 1 && a.kb0 - hz > 0) ? a.kb0 - hz : 0;
-    // this launch's share of [t_lo, kb0): the main launch takes everything but the
-    // previous block's slices, the tail launch those
-    const int64_t ts = a.t_begin > t_lo ? a.t_begin : t_lo;
-    const int64_t te = a.t_end;
-    const int64_t n_sl = te > ts ? te - ts : 0;
-    const int64_t n_st = (n_sl + KE - 1) / KE;
-
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (!staged && tid < a.bt)
-        nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
-    __syncthreads();
-
-    if (warp == NW) {  // ---- producer warp: lane 0 waits and arms the barrier, lane e copies row e
-        // (one warp instruction issues a stage's row copies: c4-full 1292 -> 1285 ms)
-        const uint64_t pol = l2_evict_first_policy();
-        int64_t g = 0;  // stage counter over all tiles of the CTA
-        for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-            const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
-            const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
-            const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
-            const double* src0 = a.H + mem * a.ms + q0;
-            for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
-                const int s = (int)(g % kStages);
-                const int64_t t0 = ts + gl * KE;
-                const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
-                const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
-                if (lane == 0) {
-                    if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                    FG_DCHECK(t0 >= 0 && t0 + nr <= a.h_alloc && t0 + nr <= a.kb0);
-                    FG_DCHECK(!staged || (t0 - ts + nr) * CP <= a.coef_mstride);
-                    FG_DCHECK(row_bytes <= TP * sizeof(double) && q0 + row_elems <= a.ms);
-                    mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
-                }
-                __syncwarp();  // the slot is free (lane 0 waited) before any lane copies into it
-                if (lane < nr)
-                    bulk_g2s_hint(rows + ((size_t)s * KE + lane) * RP, src0 + (t0 + lane) * a.slice_stride, row_bytes,
-                                  &full[s], pol);
-                if (staged && lane == 31)
-                    bulk_g2s(coef + (size_t)s * KE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
-            }
-        }
-        return;
-    }
-
-    // ---- consumers: warp w owns points [32w, 32w+32) of the tile
-    const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
-    const double* psi_b = a.psi + mem * a.psi_stride;
-    const int ngroups = NC / BT;  // threads per step column when filling the table
-    int64_t g = 0;
-    const uint32_t rows_s = smem_u32(rows) + (uint32_t)((warp * WP + fr) * 8), coef_s = smem_u32(coef) + (uint32_t)(fr * 8);
-    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-    const int64_t q0 = (int64_t)(tile % a.tpm) * TP;
-    double d[MT][NT][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
-    uint64_t* pend = nullptr;  // slot of the previous stage, released by the next one
-    for (int64_t gl = 0; gl < n_st; ++gl, ++g) {
-        const int64_t t0 = ts + gl * KE;
-        if (!staged && (gl * KE) % kCH == 0) {
-            // ensemble path: coefficient table for slices t0 .. t0+kCH-1 — zero it,
-            // then scatter w·ψ_b(m) over every schedule segment (no per-slice search)
-            asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
-            for (int i = tid; i < kCH * CP; i += NC) coef[i] = 0.0;
-            asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
-            const int bb = tid % BT, grp = tid / BT;
-            if (bb < a.bt && grp < ngroups) {
-                const int64_t k = a.kb0 + bb;
-                const int64_t t_hi = (t0 + kCH - 1 < te - 1) ? t0 + kCH - 1 : te - 1;
-                const int64_t m_lo = k - t_hi, m_hi = k - t0;  // offsets mapping into this table
-                const FgSeg* sg = segs + bb * kBlkSegs;
-                for (int si = 0; si < nseg[bb]; ++si) {
-                    const int64_t m0 = sg[si].m0, st = sg[si].stride, last = m0 + (sg[si].count - 1) * st;
-                    const int64_t lo = m_lo > m0 ? m_lo : m0, hi = m_hi < last ? m_hi : last;
-                    if (lo > hi) continue;
-                    const int64_t i0 = (lo - m0 + st - 1) / st, i1 = (hi - m0) / st;
-                    for (int64_t i = i0 + grp; i <= i1; i += ngroups) {
-                        const int64_t m = m0 + i * st;
-                        coef[(k - m - t0) * CP + bb] = __dmul_rn((double)st, __ldg(psi_b + m));
-                    }
-                }
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
-        }
-        const int s = (int)(g % kStages);
-        mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
-        const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
-        const uint32_t rs = rows_s + (uint32_t)(s * KE * RP * 8);
-        const uint32_t cs = staged ? coef_s + (uint32_t)(s * KE * CP * 8) : coef_s + (uint32_t)(((gl * KE) % kCH) * CP * 8);
-        if constexpr (LEAN) {
-        // one k-step (4 slices) of fragments live at a time, so 8 consumer warps
-        // of 32 points fit two CTAs per SM (the fp64 tensor pipe needs 16 issuing
-        // warps per SM, scripts/micro/dense_consumer.cu); the previous stage's slot
-        // is released after the first k-step's DMMAs: the dependency is on a DMMA
-        // issued after every DMMA that read the slot (so those reads are done),
-        // and 16 DMMAs old by the time the release needs it.  Stages of 16 slices
-        // (4 k-steps, not unrolled: registers) halve the barrier round trips per
-        // DMMA (c4-full 1310 -> 1277 ms, c3-full 633 -> 616)
-#pragma unroll 1
-        for (int ks = 0; ks < KE / 4; ++ks) {
-            const int e = ks * 4 + fk;
-            double af[MT], bf[NT];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) af[i] = e < nr ? lds_f64(cs + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
-#pragma unroll
-            for (int j = 0; j < NT; ++j) bf[j] = e < nr ? lds_f64(rs + (uint32_t)((e * RP + 8 * j) * 8)) : 0.0;
-            if (ks == 1) {
-                if (pend && lane == 0) mbar_arrive_after(pend, d[0][0][0], sink + warp);
-                pend = &empty[s];
-            }
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
-        }
-        } else {
-        // all fragments of the stage into registers first (partial last stage masked) ...
-        double af[KE / 4][MT], bf[KE / 4][NT];
-#pragma unroll
-        for (int ks = 0; ks < KE / 4; ++ks) {
-            const int e = ks * 4 + fk;
-#pragma unroll
-            for (int i = 0; i < MT; ++i) af[ks][i] = e < nr ? lds_f64(cs + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
-#pragma unroll
-            for (int j = 0; j < NT; ++j) bf[ks][j] = e < nr ? lds_f64(rs + (uint32_t)((e * RP + 8 * j) * 8)) : 0.0;
-        }
-        // ... then release the PREVIOUS stage's slot: the release depends on that
-        // stage's last DMMA result, and that DMMA (like every one before it) only
-        // issued once the fragments it read from the slot were in registers —
-        // so the producer's next bulk copy cannot overwrite rows still being read
-        if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1], sink + warp);
-        pend = &empty[s];
-#pragma unroll
-        for (int ks = 0; ks < KE / 4; ++ks)
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
-        }
-    }
-    // the tile's last stage: released once its DMMAs are done (the flush needs them anyway)
-    if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1], sink + warp);
-    // D fragment: row = step fr (+8 per M tile), columns = 2 adjacent points
-    double* pout = a.P + mem * a.ms + q0 + warp * WP + fk * 2;
-    FG_DCHECK(a.bt <= a.tblock && a.bt <= BT);
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        const int bb = 8 * i + fr;
-        if (bb >= a.bt) continue;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            const int64_t q = q0 + warp * WP + 8 * j + fk * 2;
-            if (q >= a.n_m) continue;
-            double* o = pout + bb * a.slice_stride + 8 * j;
-            if (a.accumulate) {
-                const double2 old = ld_cg2(o);
-                st_pair(o, __dadd_rn(old.x, d[i][j][0]), __dadd_rn(old.y, d[i][j][1]));
-            } else {
-                st_pair(o, d[i][j][0], d[i][j][1]);
-            }
-        }
-    }
-    }  // tiles
-}
-
-// ------------------------------------------- class-decomposed block stage ---
-// A thinned (adaptive) schedule samples offsets m with stride s inside each
-// interval, so in a block only the steps b with kb0+b-t ≡ m0 (mod s) use slice
-// t: the dense [BT x slices] coefficient tile above is mostly zeros (c2: ~1 in
-// 9 nonzero) and the fp64 tensor pipe, not HBM, bounds the main launch.  Here
-// the block's (step, slice) pairs of the main range are partitioned into
-// items = (stride s, residue t mod s): an item streams its slices t_first +
-// j*s (every slice of the block's union is read by exactly the items that use
-// it — one for most slices) and multiplies them with a dense coefficient tile
-// over only its own steps (≈ BT/s), so the work executed is the schedule's
-// terms rounded up to 8-step DMMA tiles.  One CTA per tile walks the items in
-// table order and adds each item's partial sums into the tile's P rows (first
-// item of a step stores), so the sums are deterministic without atomics.  Full
-// and short memory (one class holding every step) keep the dense kernel.
-
-constexpr int kMaxItems = 160;
-constexpr int kItemCols = 16;   // steps per item: two DMMA M tiles, so the kernel's
-                                // accumulators (and registers) do not grow with tblock
-constexpr int kItemPitch = kItemCols + 4;  // coefficient row pitch: 20 ≡ 4 (mod 16) doubles, conflict-free
-                                           // A-fragment loads (see coef_pitch)
-constexpr int kItemPitch8 = 12;            // 8-column items (fg_block_item8_kernel): 12 ≡ -4 (mod 16)
-
-struct BlockItem {
-    int64_t t_first;
-    int32_t stride, n_slices;
-    int32_t coef_row;  // first coefficient row (kCoefRow doubles each) of this item
-    int32_t first_mask;  // bit c: this item is the first (in table order) to add to step col2step[c]
-    int32_t ncols;     // steps in the item (<= kItemCols); column c is step col2step[c]
-    uint8_t col2step[kItemCols];
-    uint8_t map;       // 16-column kernel: its stride's tensor map in ItemMaps
-};
-
-struct ItemTable {
-    int32_t n_items;
-    int32_t accumulate;  // tail launch: every item adds to P (no first stores, no zeroing)
-    int32_t cols;        // item width of this table: 8 (fg_block_item8_kernel) or 16
-    int32_t pitch;       // its coefficient row pitch: kItemPitch8 or kItemPitch
-    uint64_t zero_mask[kMaxTBlock / 64];  // main launch: steps no item touches (their P rows are zeroed)
-    BlockItem it[kMaxItems];
-};
-
-// 16-column item kernel: one TMA tensor map per distinct item stride s, a 4-D
-// view [J][s][chunks][16] of the history (dims innermost first: 16 points,
-// B·ms/16 chunks of 128 bytes, residue t mod s, j = t div s), box {16, C, 1, kE}
-// with the 128-byte swizzle.  Built on the host per launch (encode_item_maps).
-constexpr int kMaxMaps = 16;
-struct ItemMaps {
-    CUtensorMap map[kMaxMaps];
-    CUtensorMap half[kMaxMaps];     // the same views with boxes of kIR/2 and kIR/4 slices: an
-    CUtensorMap quarter[kMaxMaps];  // item's short last stage reads its rows rounded up to kIR/4
-};
-
-// Coefficient rows of every item: row (coef_row + j), column c =
-// w·ψ(kb0 + col2step[c] - t_j) when that offset is in step col2step[c]'s
-// schedule with weight w == the item's stride (the entry belongs to this
-// item), else 0; columns ncols..CP-1 are zero padding for the DMMA tiles.
-// Ensembles (the schedule is shared, ψ is per member): blockIdx.z takes every
-// gridDim.z-th member; the entry's offset and weight are found once and reused
-// for each of its members' rows.
-__global__ void fg_item_coef_kernel(const BlockArgs a, const __grid_constant__ ItemTable T,
-                                    double* __restrict__ out, int64_t n_members) {
-    const int CP = T.pitch;
-    __shared__ FgSeg segs[kItemCols][kBlkSegs];
-    __shared__ int nseg[kItemCols];
-    const BlockItem& it = T.it[blockIdx.y];
-    const int64_t hz = a.kind == 1 ? a.horizon[0] : 0;
-    if (threadIdx.x < it.ncols) {
-        const int b = it.col2step[threadIdx.x];
-        nseg[threadIdx.x] = fg_segments(a.kind, a.kb0 + b, a.base, hz, segs[threadIdx.x], kBlkSegs);
-    }
-    __syncthreads();
-    const int64_t rows = it.n_slices;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * CP;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = e / CP;
-        const int c = (int)(e - j * CP);
-        int64_t m = -1;
-        int32_t w = 0;
-        if (c < it.ncols) {
-            m = a.kb0 + it.col2step[c] - (it.t_first + j * it.stride);
-            w = fg_seg_weight(segs[c], nseg[c], m);
-        }
-        const bool on = w == it.stride;
-        FG_DCHECK(((int64_t)it.coef_row + j + 1) * CP <= a.coef_mstride && (!on || (m >= 1 && m < a.psi_stride)));
-        double* o = out + ((int64_t)it.coef_row + j) * CP + c;
-        for (int64_t mem = blockIdx.z; mem < n_members; mem += gridDim.z)
-            o[mem * a.coef_mstride] = on ? __dmul_rn((double)w, __ldg(a.psi + mem * a.psi_stride + m)) : 0.0;
-    }
-}
-
-// One ring stage of an item with MTE live M tiles: fragments of the stage's
-// kE slices into registers, release the slot (after the reads, see
-// fg_block_tma_kernel), then MTE x NT x 2 DMMAs.
-template <int MTE, int MT, int NT, int CP, int RP>
-__device__ __forceinline__ void item_stage(double (&d)[MT][NT][2], const double* cs, const double* rs, int nr, int fk,
-                                           int lane, uint64_t* empty_s, double* sink_w) {
-    double af[kE / 4][MTE], bf[kE / 4][NT];
-    uint32_t xr = 0;
-#pragma unroll
-    for (int ks = 0; ks < kE / 4; ++ks) {
-        const int e = ks * 4 + fk;
-#pragma unroll
-        for (int i = 0; i < MTE; ++i) {
-            af[ks][i] = e < nr ? cs[e * CP + 8 * i] : 0.0;
-            const unsigned long long w = (unsigned long long)__double_as_longlong(af[ks][i]);
-            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
-        }
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            bf[ks][j] = e < nr ? rs[e * RP + 8 * j] : 0.0;
-            const unsigned long long w = (unsigned long long)__double_as_longlong(bf[ks][j]);
-            xr ^= (uint32_t)w ^ (uint32_t)(w >> 32);
-        }
-    }
-    xr = __reduce_xor_sync(0xffffffffu, xr);
-    if (lane == 0) mbar_arrive_after(empty_s, (double)xr, sink_w);
-#pragma unroll
-    for (int ks = 0; ks < kE / 4; ++ks)
-#pragma unroll
-        for (int i = 0; i < MTE; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
-}
-
-// ---- 8-column items (fg_block_item8_kernel): warps of 32 points, one DMMA M
-// tile.  Wider tiles per CTA (TP 128..256) than the 16-column kernel below, so a
-// CTA walks the item table fewer times: measured faster for a single small
-// field (c2: 22.9 vs 31.9 ms of block stage at tblock 64), while 16-column items
-// win when a class has more than 8 steps in a block (c5 at tblock 128).
-// One CTA per tile walks every item in table order through one TMA ring (the
-// ring of fg_block_tma_kernel with staged coefficient rows; the pipeline does
-// not drain between items): an item's slices are t_first + j*stride, DMMA M
-// tiles beyond its steps are skipped, and its partial sums are flushed from the
-// accumulators when its last stage is done.
-// ENS: ensembles (tpm tiles per member, per-member coefficient rows); the
-// single-member variant keeps the simpler addressing (and its registers).
-template <int TP, int NS, bool ENS>
-__global__ void __launch_bounds__(TP + 32, 4)  // <= 64 registers: two CTAs leave room for two step CTAs
-    fg_block_item8_kernel(const BlockArgs a, const __grid_constant__ ItemTable T) {
-    constexpr int kStages = NS;
-    constexpr int RP = row_pitch<TP>();
-    constexpr int CP = kItemPitch8;
-    constexpr int MT = 1;
-    constexpr int NT = 4;
-    constexpr int NW = TP / 32;
-    extern __shared__ __align__(128) unsigned char smem[];
-    double* rows = reinterpret_cast<double*>(smem);                        // [kStages][kE][RP]
-    double* coef = rows + kStages * kE * RP;                              // [kStages*kE][CP]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kE * CP);
-    uint64_t* empty = full + kStages;
-    double* sink = reinterpret_cast<double*>(empty + kStages);
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    if (warp == NW) {  // producer
-        if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            int64_t g = 0;  // stage counter over all tiles and items
-            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-            const int64_t mem = ENS ? tile / a.tpm : 0;  // ensembles: tpm tiles per member
-            const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;
-            const int64_t row_elems = (a.ms - qm) < TP ? (a.ms - qm) : TP;
-            const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
-            for (int x = blockIdx.y; x < T.n_items; x += gridDim.y) {
-                const BlockItem& it = T.it[x];
-                const double* src0 = a.H + mem * a.ms + qm + it.t_first * a.slice_stride;
-                const int64_t sstride = (int64_t)it.stride * a.slice_stride;
-                const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
-                for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
-                    const int s = (int)(g % kStages);
-                    if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                    const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
-                    const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
-                    FG_DCHECK(it.t_first + (j0 + nr - 1) * it.stride < a.h_alloc && it.t_first >= 0);
-                    FG_DCHECK(((int64_t)it.coef_row + j0 + nr) * CP <= a.coef_mstride);
-                    mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
-                    for (int e = 0; e < nr; ++e)
-                        bulk_g2s_hint(rows + ((size_t)s * kE + e) * RP, src0 + (j0 + e) * sstride, row_bytes,
-                                      &full[s], pol);
-                    bulk_g2s(coef + (size_t)s * kE * CP, c0 + j0 * CP, cbytes, &full[s]);
-                }
-            }
-            }  // tiles
-        }
-        return;
-    }
-
-    const int fr = lane >> 2, fk = lane & 3;
-    double d[MT][NT][2];
-    int64_t g = 0;
-    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-    const int64_t mem = ENS ? tile / a.tpm : 0;
-    const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;  // tile's first point within its member
-    double* const Pm = ENS ? a.P + mem * a.ms : a.P;         // member's rows of P
-    if (!T.accumulate) {  // steps no item adds to: P = 0 (this CTA owns the tile)
-        for (int w = 0; w < kMaxTBlock / 64; ++w)
-        for (uint64_t zm = T.zero_mask[w]; zm; zm &= zm - 1) {
-            const int b = 64 * w + __ffsll((long long)zm) - 1;
-            for (int i = tid; i < TP / 2; i += TP) {
-                const int64_t q = qm + 2 * i;
-                if (q < a.n_m) st_pair(Pm + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
-            }
-        }
-    }
-    for (int x = blockIdx.y; x < T.n_items; x += gridDim.y) {
-        const BlockItem& it = T.it[x];
-        const int mt = (it.ncols + 7) >> 3;
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
-        for (int64_t j0 = 0; j0 < it.n_slices; j0 += kE, ++g) {
-            const int s = (int)(g % kStages);
-            mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
-            const int nr = (int)((it.n_slices - j0) < kE ? (it.n_slices - j0) : kE);
-            const double* rs = rows + (size_t)s * kE * RP + warp * 32 + fr;
-            const double* cs = coef + (size_t)s * kE * CP + fr;
-            // warp-uniform branch per item: only the item's M tiles are issued
-            // (predicated-off DMMAs would still occupy the fp64 tensor pipe)
-            item_stage<1, MT, NT, CP, RP>(d, cs, rs, nr, fk, lane, &empty[s], sink + warp);
-        }
-        const uint64_t keep = l2_policy_last();  // the steps read P next
-        // flush into P (this CTA owns the tile, items in table order, so the
-        // sum of each step is deterministic): the first item of a step stores,
-        // later ones (and every tail item) add — loads first, one round trip.
-        // A step's row can sit in another lane than in the previous item (only
-        // this warp touches these points): the warp barrier orders the accesses.
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const int r = 8 * i + fr;
-            if (i >= mt || r >= it.ncols) continue;
-            FG_DCHECK(it.col2step[r] < a.bt && a.bt <= a.tblock);
-            double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
-            const bool add = T.accumulate || !((it.first_mask >> r) & 1);
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const int64_t q = qm + warp * 32 + 8 * j + fk * 2;
-                if (q >= a.n_m) continue;
-                if (add) {  // fire-and-forget L2 adds, applied in program order (see red_add)
-                    red_add(out + q, d[i][j][0]);
-                    red_add(out + q + 1, d[i][j][1]);
-                } else {
-                    st_pair_hint(out + q, d[i][j][0], d[i][j][1], keep);
-                }
-            }
-        }
-    }
-    }  // tiles
-}
-
-template <int TP, int NS>
-size_t item8_block_smem() {
-    return (size_t)NS * kE * row_pitch<TP>() * sizeof(double) + (size_t)NS * kE * kItemPitch8 * sizeof(double) +
-           (2 * NS) * sizeof(uint64_t) + (TP / 32) * sizeof(double);
-}
-
-// One CTA walks its tiles, and per tile every item in table order, through one
-// TMA ring (the pipeline does not drain between items or tiles): an item's
-// slices are t_first + j*stride, and its partial sums are flushed from the
-// accumulators when its last stage is done.  An item has up to 16 step columns
-// (two DMMA M tiles), so a residue class of up to 16 steps is streamed once; a
-// warp owns 16 points of the tile (one 128-byte chunk, two N tiles), which keeps
-// the accumulators at 8 doubles per thread — TP/16 consumer warps + 1 producer
-// warp, <= 64 registers, two CTAs per SM (two step CTAs still fit beside them).
-// Items of at most 8 columns issue only the first M tile (warp-uniform branch).
-//
-// A stage (kIR slices of the item's progression × TP points) is ONE tensor copy
-// per box (cp.async.bulk.tensor.4d, SASS UTMALDG) from a 4-D view of the
-// history [J][s][chunks][16] for the item's stride s (ItemMaps): coordinates
-// (0, chunk, t mod s, t div s) select kIR slices t, t+s, … at once.  The per-row
-// bulk copies this replaces (one UBLKCP per slice row, issued through a
-// serialised uniform loop) left the producer warp issue-bound and the DRAM
-// stream at 38 % of peak (profiles/r02_c3a_item16_*).  The box lands densely in
-// shared memory with the 128-byte swizzle: line L (128 B = one warp's 16 points
-// of one slice) has its 16-byte units XORed with L mod 8, so a B-fragment load
-// (4 slices × 8 points) splits 2 + 2 over the two bank halves — the minimum of
-// two wavefronts for 32 × 8 bytes.  That needs C chunks per box with C·fk
-// mod 8 ∈ {0, 6, 4, 2} or {0, 4, 0, 4}: boxes of 6 chunks (TP 96) or two boxes
-// of 4 chunks (TP 128).
-// ENS: ensembles (tpm tiles per member, per-member coefficient rows); the
-// single-member variant keeps the simpler addressing.
-#ifndef FG_ITEM_ROWS
-#define FG_ITEM_ROWS 16
-#endif
-constexpr int kIR = FG_ITEM_ROWS;  // slices per stage of the 16-column item kernel (multiple of kE)
-static_assert(kIR % kE == 0 && kIR <= 32, "item stage rows");
-
-template <int TP>
-__host__ __device__ constexpr int item_threads() { return TP / 16 * 32 + 32; }
-template <int TP>
-__host__ __device__ constexpr int item_box_chunks() { return TP == 96 ? 6 : 4; }  // 16-point chunks per TMA box
-template <int TP>
-__host__ __device__ constexpr int item_stage_bytes() { return kIR * TP * (int)sizeof(double); }  // multiple of 1024 (swizzle atom)
-
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-
-// One ring stage of an item with MTE live M tiles: A fragments (coefficients)
-// at shared address ca (+ e·CP + 8i doubles), B fragments at the swizzled byte
-// offsets boff of the stage at ra.  FULL: all kE rows belong to the item (no
-// masking).  Before its DMMAs the warp releases the PREVIOUS stage's slot
-// (pend): the release depends on the last DMMA result of that stage, which was
-// only issued once every fragment it and the DMMAs before it read had arrived
-// in registers — so the producer cannot overwrite rows still being read, and
-// the release costs one dependent store instead of a warp-wide reduction of the
-// loaded values.
-template <int MTE, int MT, int NT, int CP, bool FULL>
-__device__ __forceinline__ void item_stage_sw(double (&d)[MT][NT][2], uint32_t ca, uint32_t ra,
-                                              const uint32_t (&boff)[kE / 4][NT], int nr, int fk, int lane,
-                                              uint64_t* pend, double* sink_w) {
-    double af[kE / 4][MTE], bf[kE / 4][NT];
-#pragma unroll
-    for (int ks = 0; ks < kE / 4; ++ks) {
-        const int e = ks * 4 + fk;
-#pragma unroll
-        for (int i = 0; i < MTE; ++i)
-            af[ks][i] = (FULL || e < nr) ? lds_f64(ca + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
-#pragma unroll
-        for (int j = 0; j < NT; ++j)  // rows past the item's end hold other (or unwritten) slices: masked
-            bf[ks][j] = (FULL || e < nr) ? lds_f64(ra + boff[ks][j]) : 0.0;
-    }
-    // the previous stage of this item had the same MTE: its last DMMA wrote d[MTE - 1][NT - 1]
-    // (a register dependency only: an add here would take a slot of the fp64 pipe)
-    if (pend && lane == 0) mbar_arrive_after(pend, d[MTE - 1][NT - 1][1], sink_w);
-#pragma unroll
-    for (int ks = 0; ks < kE / 4; ++ks)
-#pragma unroll
-        for (int i = 0; i < MTE; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[ks][i], bf[ks][j]);
-}
-
-template <int TP, int NS, bool ENS>
-__global__ void __maxnreg__(64)  // <= 64 registers: two step CTAs fit beside two of these per SM
-    fg_block_item_kernel(const BlockArgs a, const __grid_constant__ ItemTable T, const __grid_constant__ ItemMaps M) {
-    constexpr int kStages = NS;
-    constexpr int CP = kItemPitch;
-    constexpr int MT = 2;
-    constexpr int NT = 2;
-    constexpr int NW = TP / 16;
-    constexpr int C = item_box_chunks<TP>();
-    constexpr int NB = NW / C;                       // boxes per stage
-    constexpr int SB = item_stage_bytes<TP>();
-    constexpr int BOXB = C * kIR * 128;              // bytes per box
-    static_assert(NB * C == NW && SB % 1024 == 0 && BOXB % 1024 == 0, "item tile / box geometry");
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    // swizzle-128B boxes need 1024-byte aligned destinations (1 KB of slack is allocated)
-    unsigned char* rows = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // [kStages][SB]
-    double* coef = reinterpret_cast<double*>(rows + (size_t)kStages * SB);              // [kStages*kIR][CP]
-    uint64_t* full = reinterpret_cast<uint64_t*>(coef + kStages * kIR * CP);
-    uint64_t* empty = full + kStages;
-    double* sink = reinterpret_cast<double*>(empty + kStages);
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    if (warp == NW) {  // producer warp: one lane issues a stage's boxes and coefficient rows
-        if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            int64_t g = 0;  // stage counter over all tiles and items
-            for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-                const int64_t mem = ENS ? tile / a.tpm : 0;  // ensembles: tpm tiles per member
-                const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;
-                const int chunk0 = (int)((mem * a.ms + qm) >> 4);
-                for (int x = 0; x < T.n_items; ++x) {
-                    const BlockItem& it = T.it[x];
-                    const CUtensorMap* map = &M.map[it.map];
-                    const int r = (int)(it.t_first % it.stride);
-                    const int j_first = (int)(it.t_first / it.stride);
-                    const double* c0 = a.gcoef + (ENS ? mem * a.coef_mstride : 0) + (int64_t)it.coef_row * CP;
-                    for (int64_t j0 = 0; j0 < it.n_slices; j0 += kIR, ++g) {
-                        const int s = (int)(g % kStages);
-                        const int nr = (int)((it.n_slices - j0) < kIR ? (it.n_slices - j0) : kIR);
-                        if (g >= kStages) mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
-                        const uint32_t cbytes = (uint32_t)(nr * CP * sizeof(double));
-                        // the box reads kIR slices of the progression: all of them allocated
-                        FG_DCHECK(it.t_first + (j0 + kIR - 1) * (int64_t)it.stride < a.h_alloc && it.t_first >= 0);
-                        FG_DCHECK(it.t_first + (j0 + nr - 1) * (int64_t)it.stride < a.kb0 + a.bt);
-                        FG_DCHECK(((int64_t)it.coef_row + j0 + nr) * CP <= a.coef_mstride);
-                        // a box may run past the member (partial last tile: its points are never
-                        // stored) or past the history (the TMA zero-fills); it starts inside
-                        FG_DCHECK(it.map < kMaxMaps && chunk0 < a.slice_stride / 16);
-                        // a short last stage is covered by half- and quarter-depth boxes
-                        // (rows rounded up to kIR/4), landing on the same rows of the box
-                        // slots as the full box would (the consumers never read past nr)
-                        const int rows_rd = nr == kIR ? kIR : nr > kIR / 2 + kIR / 4 ? kIR : (nr + kIR / 4 - 1) / (kIR / 4) * (kIR / 4);
-                        mbar_expect_tx(&full[s], (uint32_t)(SB / kIR * rows_rd) + cbytes);
-                        for (int e0 = 0; e0 < rows_rd;) {
-                            const int depth = rows_rd - e0 >= kIR ? kIR : rows_rd - e0 >= kIR / 2 ? kIR / 2 : kIR / 4;
-                            const CUtensorMap* mp = depth == kIR ? map : depth == kIR / 2 ? &M.half[it.map]
-                                                                                          : &M.quarter[it.map];
-#pragma unroll
-                            for (int b = 0; b < NB; ++b)
-                                tma_load_4d(rows + (size_t)s * SB + b * BOXB + e0 * C * 128, mp, 0, chunk0 + b * C, r,
-                                            j_first + (int)j0 + e0, &full[s], pol);
-                            e0 += depth;
-                        }
-                        bulk_g2s(coef + (size_t)s * kIR * CP, c0 + j0 * CP, cbytes, &full[s]);
-                    }
-                }
-            }  // tiles
-        }
-        return;
-    }
-
-    const int fr = lane >> 2, fk = lane & 3;
-    // byte offsets of this lane's B fragments in a stage: slice e = 4ks + fk,
-    // point 16·warp + 8j + fr → box warp / C, line L = e·C + warp % C, 16-byte
-    // unit (4j + fr/2) XOR (L mod 8), half (fr & 1)
-    uint32_t boff[kE / 4][NT];
-#pragma unroll
-    for (int ks = 0; ks < kE / 4; ++ks)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            const int L = (ks * 4 + fk) * C + warp % C;
-            const int u = (4 * j + (fr >> 1)) ^ (L & 7);
-            boff[ks][j] = (uint32_t)((warp / C) * BOXB + L * 128 + u * 16 + (fr & 1) * 8);
-        }
-    const uint32_t rows_s = smem_u32(rows), coef_s = smem_u32(coef) + (uint32_t)(fr * 8);
-    double d[MT][NT][2];
-    int64_t g = 0;
-    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-    const int64_t mem = ENS ? tile / a.tpm : 0;
-    const int64_t qm = (int64_t)(tile - mem * a.tpm) * TP;  // tile's first point within its member
-    double* const Pm = ENS ? a.P + mem * a.ms : a.P;         // member's rows of P
-    if (!T.accumulate) {  // steps no item adds to: P = 0 (this CTA owns the tile)
-        for (int w = 0; w < kMaxTBlock / 64; ++w)
-        for (uint64_t zm = T.zero_mask[w]; zm; zm &= zm - 1) {
-            const int b = 64 * w + __ffsll((long long)zm) - 1;
-            for (int i = tid; i < TP / 2; i += NW * 32) {
-                const int64_t q = qm + 2 * i;
-                if (q < a.n_m) st_pair(Pm + (int64_t)b * a.slice_stride + q, 0.0, 0.0);
-            }
-        }
-    }
-    for (int x = 0; x < T.n_items; ++x) {
-        const BlockItem& it = T.it[x];
-        const int mt = (it.ncols + 7) >> 3;
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
-        uint64_t* pend = nullptr;  // slot of the previous stage, released by the next one
-        for (int64_t j0 = 0; j0 < it.n_slices; j0 += kIR, ++g) {
-            const int s = (int)(g % kStages);
-            mbar_wait(&full[s], (uint32_t)((g / kStages) & 1));
-            const int nr = (int)((it.n_slices - j0) < kIR ? (it.n_slices - j0) : kIR);
-            // a stage's kIR rows in groups of kE (fragment registers for kE rows
-            // only); the previous stage's slot is released after the first group's loads
-#pragma unroll
-            for (int h = 0; h < kIR / kE; ++h) {
-                const int nrh = nr - h * kE;  // rows of this group that belong to the item
-                if (nrh <= 0) break;          // warp-uniform
-                const uint32_t ra = rows_s + (uint32_t)(s * SB + h * kE * C * 128);
-                const uint32_t ca = coef_s + (uint32_t)((s * kIR + h * kE) * CP * 8);
-                uint64_t* rel = h == 0 ? pend : nullptr;
-                // warp-uniform branches per item and group: only the item's M tiles
-                // are issued (predicated-off DMMAs would still occupy the fp64 tensor
-                // pipe), and only a partial last group masks its rows
-                if (nrh >= kE) {
-                    if (mt > 1)
-                        item_stage_sw<2, MT, NT, CP, true>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
-                    else
-                        item_stage_sw<1, MT, NT, CP, true>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
-                } else {
-                    if (mt > 1)
-                        item_stage_sw<2, MT, NT, CP, false>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
-                    else
-                        item_stage_sw<1, MT, NT, CP, false>(d, ca, ra, boff, nrh, fk, lane, rel, sink + warp);
-                }
-            }
-            pend = &empty[s];
-        }
-        // the item's last stage: released once its DMMAs are done (the flush needs them anyway)
-        if (pend && lane == 0) mbar_arrive_after(pend, d[MT - 1][NT - 1][1] + d[0][NT - 1][1], sink + warp);
-        const uint64_t keep = l2_policy_last();  // the steps read P next
-        // flush into P (this CTA owns the tile, items in table order, so the
-        // sum of each step is deterministic): the first item of a step stores,
-        // later ones (and every tail item) add.  A step's row can sit in another
-        // lane than in the previous item (only this warp touches these points):
-        // the warp barrier orders the accesses.
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const int r = 8 * i + fr;
-            if (i >= mt || r >= it.ncols) continue;
-            FG_DCHECK(it.col2step[r] < a.bt && a.bt <= a.tblock);
-            double* out = Pm + (int64_t)it.col2step[r] * a.slice_stride;
-            const bool add = T.accumulate || !((it.first_mask >> r) & 1);
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const int64_t q = qm + warp * 16 + 8 * j + fk * 2;
-                if (q >= a.n_m) continue;
-                if (add) {  // fire-and-forget L2 adds, applied in program order (see red_add)
-                    red_add(out + q, d[i][j][0]);
-                    red_add(out + q + 1, d[i][j][1]);
-                } else {
-                    st_pair_hint(out + q, d[i][j][0], d[i][j][1], keep);
-                }
-            }
-        }
-    }
-    }  // tiles
-}
-
-template <int TP, int NS>
-size_t item_block_smem() {
-    return 1024 + (size_t)NS * item_stage_bytes<TP>() + (size_t)NS * kIR * kItemPitch * sizeof(double) +
-           (2 * NS) * sizeof(uint64_t) + (TP / 16) * sizeof(double);
-}
-
-// ------------------------------------------------------------------ ψ tables ---
-// coefficients.py:86-91: v = ((-v) * ((2 - γ) - m)) / m, each op rounded once.
-__global__ void fg_psi_kernel(const double* __restrict__ gamma, int64_t B, int64_t n, int64_t stride,
-                              double* __restrict__ out) {
-    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    const double g = gamma[b];
-    const double two_minus_g = __dsub_rn(2.0, g);
-    double* o = out + b * stride;
-    double v = 1.0;
-    o[0] = v;
-    for (int64_t m = 1; m <= n; ++m) {
-        const double fm = (double)m;
-        v = __ddiv_rn(__dmul_rn(-v, __dsub_rn(two_minus_g, fm)), fm);
-        o[m] = v;
-    }
-}
-
-// ----------------------------------------------------------- schedule expand ---
-__global__ void fg_schedule_kernel(int kind, int64_t k0, int64_t base, int64_t horizon, int32_t* offs,
-                                   int32_t* wts, int64_t row_cap, int64_t* lens) {
-    __shared__ FgSeg segs[FG_MAX_SEGS];
-    __shared__ int64_t first[FG_MAX_SEGS + 1];
-    __shared__ int s_n;
-    const int64_t k = k0 + blockIdx.x;
-    if (threadIdx.x == 0) {
-        int n = fg_segments(kind, k, base, horizon, segs);
-        int64_t acc = 0;
-        for (int i = 0; i < n; ++i) {
-            first[i] = acc;
-            acc += segs[i].count;
-        }
-        first[n > 0 ? n : 0] = acc;
-        s_n = n;
-        lens[blockIdx.x] = n > 0 ? acc : -1;
-    }
-    __syncthreads();
-    const int n = s_n;
-    if (n <= 0) return;
-    const int64_t len = first[n];
-    const int64_t lim = len < row_cap ? len : row_cap;
-    int32_t* orow = offs + (int64_t)blockIdx.x * row_cap;
-    int32_t* wrow = wts + (int64_t)blockIdx.x * row_cap;
-    for (int64_t j = threadIdx.x; j < lim; j += blockDim.x) {
-        int si = 0;
-        while (si + 1 < n && first[si + 1] <= j) ++si;
-        orow[j] = (int32_t)(segs[si].m0 + (j - first[si]) * segs[si].stride);
-        wrow[j] = (int32_t)segs[si].stride;
-    }
-}
-
-// -------------------------------------------------------- generic history_sum ---
-__global__ void fg_history_sum_kernel(const double* __restrict__ H, int64_t ss, int64_t n,
-                                      const int64_t* __restrict__ offs, const int64_t* __restrict__ wts,
-                                      int64_t len, const double* __restrict__ psi, int64_t k,
-                                      double* __restrict__ out) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    double acc = 0.0;
-    for (int64_t j = 0; j < len; ++j) {
-        const int64_t m = offs[j];
-        const double c = __dmul_rn((double)wts[j], psi[m]);
-        acc = fma(c, H[(k - m) * ss + p], acc);
-    }
-    out[p] = acc;
-}
-
-// ------------------------------------------------------------ plain stencil ---
-template <int NDIM>
-__global__ void fg_stencil_kernel(const double* __restrict__ u, double* __restrict__ out, int64_t B,
-                                  int64_t ms, int32_t n_m, Shape sh) {
-    const int64_t b = blockIdx.y;
-    const int32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n_m) return;
-    const double* ub = u + b * ms;
-    out[b * ms + q] = delta_at<NDIM>(ub, sh, q, ub[q]);
-}
 
 // ------------------------------------------------------------------ host side ---
 
@@ -2216,7 +247,7 @@ int launch_single(const fg_plan* p, int64_t k, double* snap, cudaStream_t st, in
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.total_tiles, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = acc_smem(s, 1);
+    cfg.dynamicSmemBytes = (kb0 >= 0 && s == 1) ? 0 : acc_smem(s, 1);  // BLK: the sum stays in registers
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     if (pdl_wait) {
