@@ -130,8 +130,22 @@ def exchange_halos(rows, layout: SlabLayout) -> None:
 
     if layout.world == 1:
         return
+    plan = layout.exchange_plan()
+    if rows.is_cuda and dist.get_backend() == "gloo":
+        # gloo moves host memory only: stage the edge rows through the host (the
+        # one-GPU test of the slab path; ranks on real GPUs use NCCL below)
+        bufs = {(op, peer, tag): (rows[row].cpu() if op == "send" else rows[row].new_empty(rows[row].shape, device="cpu"))
+                for op, peer, row, tag in plan}
+        ops = [dist.P2POp(dist.isend if op == "send" else dist.irecv, bufs[(op, peer, tag)], peer, tag=tag)
+               for op, peer, _, tag in plan]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for op, peer, row, tag in plan:
+            if op == "recv":
+                rows[row].copy_(bufs[(op, peer, tag)])
+        return
     ops = []
-    for op, peer, row, tag in layout.exchange_plan():
+    for op, peer, row, tag in plan:
         fn = dist.isend if op == "send" else dist.irecv
         ops.append(dist.P2POp(fn, rows[row], peer, tag=tag))
     for req in dist.batch_isend_irecv(ops):
@@ -152,8 +166,13 @@ def gather_rows(own, layout: SlabLayout, device=None):
     big = max(hi - lo for lo, hi in counts)
     pad = torch.zeros((big,) + tuple(width), dtype=own.dtype, device=own.device)
     pad[: own.shape[0]] = own
-    bufs = [torch.empty_like(pad) for _ in counts]
-    dist.all_gather(bufs, pad)
+    if pad.is_cuda and dist.get_backend() == "gloo":  # host-staged (see exchange_halos)
+        hb = [torch.empty_like(pad, device="cpu") for _ in counts]
+        dist.all_gather(hb, pad.cpu())
+        bufs = [b.to(pad.device) for b in hb]
+    else:
+        bufs = [torch.empty_like(pad) for _ in counts]
+        dist.all_gather(bufs, pad)
     for i, (lo, hi) in enumerate(counts):
         parts[i].copy_(bufs[i][: hi - lo])
     return torch.cat(parts, 0)
@@ -199,6 +218,8 @@ def run_slabs(cfg, device=None):
     torch.cuda.synchronize(device)
     bad = torch.tensor([st.first_bad_step() or (1 << 62)], dtype=torch.int64, device=st.device)
     if world > 1:
+        if dist.get_backend() == "gloo":
+            bad = bad.cpu()
         dist.all_reduce(bad, op=dist.ReduceOp.MIN)
     out = [(0, np.asarray(p.u0))]
     for s in sorted(snaps):

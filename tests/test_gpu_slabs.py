@@ -1,10 +1,11 @@
 """Slab-sharded single-field runs on the GPU.
 
 World size 1 runs the per-step slab driver (one advance per step, halo exchange
-a no-op) and must reproduce the engine's own run bit for bit.  The 2-rank NCCL
-run needs two GPUs: it is launched with torchrun when they are present and
-skipped otherwise (the round's boxes have one GPU; the host logic is proven
-with gloo in tests/test_dist.py).
+a no-op) and must reproduce the engine's own run bit for bit.  Two ranks with
+real halos run on the one GPU over gloo (edge rows staged through the host).
+The 2-rank NCCL run needs two GPUs: it is launched with torchrun when they are
+present and skipped otherwise (the host logic is also proven with gloo and the
+oracle's arithmetic in tests/test_dist.py).
 """
 
 import os
@@ -48,9 +49,16 @@ def _worker_main():
     from paper_1004_5128_b200.sharding import run_slabs
 
     rank = int(os.environ["RANK"])
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", device_id=dev)
+    if os.environ.get("FGB200_SLAB_TEST_BACKEND") == "gloo":
+        # both ranks on cuda:0, halos staged through the host: the ranks' kernels
+        # never wait on one another (each exchange is host-synchronised)
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", device_id=dev)
     cfg = _cfg()
     snaps, bad = run_slabs(cfg, device=dev)
     if rank == 0:
@@ -59,6 +67,18 @@ def _worker_main():
         assert bad is None and worst <= 1e-10, worst
         print("slab parity ok", worst)
     dist.destroy_process_group()
+
+
+def test_slab_two_ranks_one_gpu_gloo(cuda_device):
+    """The 2-rank slab path with real halos on ONE GPU: two processes share
+    cuda:0, every rank runs the engine on its slab, edge rows travel over gloo
+    through the host.  Same layout, plan and gather as the NCCL run."""
+    env = dict(os.environ, FGB200_SLAB_TEST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29534", os.path.abspath(__file__)]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    assert "slab parity ok" in res.stdout
 
 
 def test_slab_two_ranks_nccl(cuda_device):
