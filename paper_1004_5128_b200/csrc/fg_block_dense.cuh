@@ -127,13 +127,29 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 #ifndef FG_STAGED_RING
 #define FG_STAGED_RING 6
 #endif
+#ifndef FG_TAIL_STAGES
+#define FG_TAIL_STAGES 2
+#endif
+#ifndef FG_DENSE_SOLO
+#define FG_DENSE_SOLO 1   // large-field BT = 32 main launches: one 128-register CTA per SM (0: two 96-register CTAs)
+#endif
+#ifndef FG_DENSE_TAIL_RED
+#define FG_DENSE_TAIL_RED 0
+#endif
+#ifndef FG_SOLO_FOLD
+#define FG_SOLO_FOLD 0
+#endif
+#ifndef FG_SOLO_LB
+#define FG_SOLO_LB 0
+#endif
+#ifndef FG_SOLO_REGS
+#define FG_SOLO_REGS 128
+#endif
+constexpr int kSoloStages = 4;  // ring of the solo main launch: 4 stages of 16 slices (two CTAs: 3)
 template <bool STAGED>
 __host__ __device__ constexpr int ring_stages() { return STAGED ? FG_STAGED_RING : 4; }
 
 constexpr int kMainStages = FG_STAGED_RING;  // staged main launches
-#ifndef FG_TAIL_STAGES
-#define FG_TAIL_STAGES 2
-#endif
 constexpr int kTailStages = FG_TAIL_STAGES;  // tail launches: small ring, so they fit beside two main CTAs per SM
 
 // slice rows per stage of the dense kernel: 16 for the 4-M-tile blocks (lean
@@ -211,8 +227,8 @@ __global__ void fg_block_coef_kernel(const BlockArgs a, double* __restrict__ out
 // a CTA can have twice the warps (measured: the fp64 tensor pipe reaches its
 // peak only with 4 issuing warps per SM sub-partition, 16 per SM —
 // scripts/micro/dense_consumer.cu; 7-warp CTAs stop at 7/8 of it).
-template <int BT, int TP, bool STAGED, int NS, int WP>
-__global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+template <int BT, int TP, bool STAGED, int NS, int WP, bool SOLO>
+__device__ __forceinline__ void fg_block_tma_body(const BlockArgs& a) {
     constexpr int kStages = NS;
     constexpr int KE = dense_ke<BT>();  // slice rows per stage
     static_assert(KE < 32, "one producer lane per stage row, lane 31 copies the coefficient rows");
@@ -263,7 +279,40 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
     __syncthreads();
 
-    if (warp == NW) {  // ---- producer warp: lane 0 waits and arms the barrier, lane e copies row e
+    // FOLD (solo launches): no producer warp — consumer warp 0 issues stage g-1+kStages
+    // after its third k-step of stage g, when every warp has released stage g-1's
+    // slot, so the CTA is 8 warps (two per SM sub-partition) and two step CTAs fit
+    // beside it instead of one
+    constexpr bool FOLD = SOLO && FG_SOLO_FOLD;
+    const uint64_t fold_pol = FOLD ? l2_evict_first_policy() : 0;
+    auto produce = [&](int64_t pg) {  // whole warp 0; stage pg of the CTA's tile sequence
+        if (n_st == 0) return;
+        const int64_t ti = pg / n_st, gl = pg - ti * n_st;
+        const int64_t tile = blockIdx.x + ti * gridDim.x;
+        if (tile >= a.total_tiles) return;
+        const int s = (int)(pg % kStages);
+        const int64_t q0 = (tile % a.tpm) * TP;
+        const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
+        const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
+        const double* src0 = a.H + mem * a.ms + q0;
+        const int64_t t0 = ts + gl * KE;
+        const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
+        const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
+        if (lane == 0) {
+            if (pg >= kStages) mbar_wait(&empty[s], (uint32_t)(((pg / kStages) & 1) ^ 1));
+            FG_DCHECK(t0 >= 0 && t0 + nr <= a.h_alloc && t0 + nr <= a.kb0);
+            mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
+        }
+        __syncwarp();
+        if (lane < nr)
+            bulk_g2s_hint(rows + ((size_t)s * KE + lane) * RP, src0 + (t0 + lane) * a.slice_stride, row_bytes, &full[s],
+                          fold_pol);
+        if (staged && lane == 31) bulk_g2s(coef + (size_t)s * KE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
+    };
+    if (FOLD && warp == 0)
+        for (int pg = 0; pg < kStages; ++pg) produce(pg);
+
+    if (!FOLD && warp == NW) {  // ---- producer warp: lane 0 waits and arms the barrier, lane e copies row e
         // (one warp instruction issues a stage's row copies: c4-full 1292 -> 1285 ms)
         const uint64_t pol = l2_evict_first_policy();
         int64_t g = 0;  // stage counter over all tiles of the CTA
@@ -350,6 +399,38 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
         // and 16 DMMAs old by the time the release needs it.  Stages of 16 slices
         // (4 k-steps, not unrolled: registers) halve the barrier round trips per
         // DMMA (c4-full 1310 -> 1277 ms, c3-full 633 -> 616)
+        if constexpr (SOLO) {
+        // fragments of k-step ks+1 are loaded before the DMMAs of k-step ks issue
+        // (two k-steps live, 112 registers): the shared-memory latency hides
+        // behind the warp's own 16 DMMAs instead of behind other warps
+        double af[2][MT], bf[2][NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) af[0][i] = fk < nr ? lds_f64(cs + (uint32_t)((fk * CP + 8 * i) * 8)) : 0.0;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) bf[0][j] = fk < nr ? lds_f64(rs + (uint32_t)((fk * RP + 8 * j) * 8)) : 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KE / 4; ++ks) {
+            const int cur = ks & 1, nxt = cur ^ 1;
+            if (ks + 1 < KE / 4) {
+                const int e = (ks + 1) * 4 + fk;
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+                    af[nxt][i] = e < nr ? lds_f64(cs + (uint32_t)((e * CP + 8 * i) * 8)) : 0.0;
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+                    bf[nxt][j] = e < nr ? lds_f64(rs + (uint32_t)((e * RP + 8 * j) * 8)) : 0.0;
+            }
+            if (ks == 1) {
+                if (pend && lane == 0) mbar_arrive_after(pend, d[0][0][0], sink + warp);
+                pend = &empty[s];
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[cur][i], bf[cur][j]);
+            if (FOLD && ks == 2 && warp == 0 && g >= 1) produce(g - 1 + kStages);
+        }
+        } else {
 #pragma unroll 1
         for (int ks = 0; ks < KE / 4; ++ks) {
             const int e = ks * 4 + fk;
@@ -366,6 +447,7 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
             for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
+        }
         }
         } else {
         // all fragments of the stage into registers first (partial last stage masked) ...
@@ -407,14 +489,41 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
             if (q >= a.n_m) continue;
             double* o = pout + bb * a.slice_stride + 8 * j;
             if (a.accumulate) {
+#if FG_DENSE_TAIL_RED
+                // one add per element and launch: an L2 reduction rounds exactly like
+                // load-add-store and spares the consumer warp the load round trip
+                red_add(o, d[i][j][0]);
+                red_add(o + 1, d[i][j][1]);
+#else
                 const double2 old = ld_cg2(o);
                 st_pair(o, __dadd_rn(old.x, d[i][j][0]), __dadd_rn(old.y, d[i][j][1]));
+#endif
             } else {
                 st_pair(o, d[i][j][0], d[i][j][1]);
             }
         }
     }
     }  // tiles
+}
+
+// two CTAs per SM (every dense launch but the large-field main launches below)
+template <int BT, int TP, bool STAGED, int NS, int WP>
+__global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(const BlockArgs a) {
+    fg_block_tma_body<BT, TP, STAGED, NS, WP, false>(a);
+}
+
+// "Solo" main launch of large single fields at BT = 32: ONE CTA per SM with 128
+// registers per thread, so the lean consumer loop can keep two k-steps of
+// fragments live (software-pipelined, no spills) and the 8 consumer warps issue
+// DMMAs without waiting for shared memory; the second CTA's registers are left
+// to a step CTA of the block running beside it.
+template <int BT, int TP, bool STAGED, int NS, int WP>
+#if FG_SOLO_LB
+__global__ void __launch_bounds__(TP / WP * 32 + 32, 1) fg_block_tma_solo_kernel(const BlockArgs a) {
+#else
+__global__ void __maxnreg__(FG_SOLO_REGS) fg_block_tma_solo_kernel(const BlockArgs a) {
+#endif
+    fg_block_tma_body<BT, TP, STAGED, NS, WP, true>(a);
 }
 
 }  // namespace

@@ -342,6 +342,7 @@ struct BlockVariant {
     size_t smem;
     int tp;
     int threads;
+    int per_sm = 2;  // CTAs per SM of a single-member launch (grid cap)
 };
 
 template <int BT, int TP, bool ST, int NS, int WP>
@@ -387,6 +388,14 @@ BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
     // stage barrier and coefficient rows over more warps (measured c3-full at
     // tblock 32: TP 224 705 ms vs TP 192 792 ms, nearly equal balance; TP 256,
     // 16 consumer warps per SM: 662 vs 678 ms at TP 224, c4-full 1386 vs 1411 ms)
+    // large single fields, full/short memory at BT = 32: the solo main launch
+    // (one CTA per SM, fg_block_tma_solo_kernel) once every SM has several tiles
+    if (FG_DENSE_SOLO && !tail && staged && p->tblock == 32 && (p->n_m + 255) / 256 >= 4 * (int64_t)sm_count()) {
+        BlockVariant v = {fg_block_tma_solo_kernel<32, 256, true, kSoloStages, 32>,
+                          tma_block_smem<32, 256, true, kSoloStages, 32>(), 256, 256 / 32 * 32 + (FG_SOLO_FOLD ? 0 : 32)};
+        v.per_sm = 1;
+        return v;
+    }
     bool found = false;
     for (int tp : cands) {
         if (found) continue;
@@ -405,9 +414,9 @@ BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
 
 // Block-kernel grid: ensembles one CTA per tile; single members two CTAs per SM
 // looping over tiles (one wave; two step CTAs still fit beside them per SM).
-unsigned block_grid(const fg_plan* p, int64_t total_tiles) {
+unsigned block_grid(const fg_plan* p, int64_t total_tiles, int per_sm = 2) {
     if (p->B != 1) return (unsigned)total_tiles;
-    const int64_t cap = (int64_t)sm_count() * 2;
+    const int64_t cap = (int64_t)sm_count() * per_sm;
     return (unsigned)(total_tiles < cap ? total_tiles : cap);
 }
 
@@ -865,7 +874,7 @@ int launch_block_main(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
     ++g_launches;
-    v.kern<<<block_grid(p, a.total_tiles), v.threads, v.smem, st>>>(a);
+    v.kern<<<block_grid(p, a.total_tiles, v.per_sm), v.threads, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma launch");
 }
 
@@ -970,7 +979,16 @@ struct BlockTrace {
     const char* path;
     std::vector<int64_t> kb;
     std::vector<cudaEvent_t> ev;  // 5 per block
-    explicit BlockTrace(const char* p) : path(p) {}
+    std::vector<std::pair<int64_t, cudaEvent_t>> sev;  // per-step completion events (FGB200_TRACE_STEPS=1)
+    bool per_step = false;
+    explicit BlockTrace(const char* p) : path(p) { per_step = p && getenv("FGB200_TRACE_STEPS"); }
+    void step_mark(int64_t k, cudaStream_t s) {
+        if (!per_step) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        sev.emplace_back(k, e);
+    }
     void mark(int64_t k, int slot, cudaStream_t s) {
         if (!path) return;
         if (kb.empty() || kb.back() != k) {
@@ -999,6 +1017,10 @@ struct BlockTrace {
             cudaEvent_t next = i + 1 < kb.size() ? ev[(i + 1) * 5] : fin;
             fprintf(f, "%lld t=%.1f wait=%.1f tail=%.1f steps=%.1f main_next=%.1f\n", (long long)kb[i],
                     ms(ev[0], e[0]), ms(e[0], e[1]), ms(e[1], e[2]), ms(e[2], next), ms(e[3], e[4]));
+        }
+        for (auto& se : sev) {
+            if (f) fprintf(f, "step %lld done t=%.1f\n", (long long)se.first, ms(ev[0], se.second));
+            cudaEventDestroy(se.second);
         }
         if (f) fclose(f);
         for (cudaEvent_t e : ev)
@@ -1334,6 +1356,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
     int64_t si = 0;
     while (si < n_snap && snap_steps[si] <= k0) ++si;
     int rc = FG_OK;
+    BlockTrace tr(graph || !tb ? nullptr : getenv("FGB200_TRACE"));
 
     // snapshots to host: each one is copied on a library copy stream as soon as
     // the launch that produced it is done, overlapping the following steps
@@ -1371,6 +1394,7 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
                 t_min = kb0 + (b >= S + D ? S * ((b - D) / S) : 0);
             }
             if (int r = launch_single(p, k, snap, cap, wait, pdl, kb0, t_min)) return r;
+            if ((k & 3) == 3) tr.step_mark(k, cap);
             if (snap)
                 if (int r = copy_out(i, i + 1)) return r;
         }
@@ -1490,7 +1514,6 @@ int fg_run_ex(const fg_plan* p, int64_t k0, int64_t k1, const int64_t* snap_step
         if (rc == FG_OK && pairs)
             rc = cuda_check(cudaMemsetAsync(u3_step, 0xff, sizeof(int64_t), cap), "pair step reset");  // -1
         int64_t main_on_side = -1;  // block whose main launch is in flight on `side`
-        BlockTrace tr(graph ? nullptr : getenv("FGB200_TRACE"));
         for (int64_t kb = k0 - k0 % tb; kb < k1 && rc == FG_OK; kb += tb) {
             const int64_t ks = kb > k0 ? kb : k0, ke = kb + tb < k1 ? kb + tb : k1;
             // blocks are aligned to multiples of tb, so a run split into several
