@@ -388,7 +388,10 @@ class Run:
                 blk["kernel"] = f"fg_item_coef_kernel + {item} (main + tail)"
                 blk["bound"] = "hbm"
             else:
-                blk["kernel"] = "fg_block_coef_kernel + fg_block_tma_kernel (main + tail)"
+                big = st.tblock == 32 and prob.batch == 1 and -(-prob.n_m // 256) >= 4 * 148
+                blk["kernel"] = ("fg_block_coef_kernel + fg_block_tma_solo_kernel (main, one CTA per SM) + "
+                                 "fg_block_tma_kernel (tail)" if big
+                                 else "fg_block_coef_kernel + fg_block_tma_kernel (main + tail)")
                 # at tblock >= 24 a dense block does 2·tblock flops per 8 history bytes:
                 # past the fp64 tensor ridge (37 TF/s ÷ 6.45 TB/s ≈ 5.7 flop/B)
                 blk["bound"] = "tensor" if st.tblock * 2 / 8 > FP64_TENSOR_PEAK / (peak_gbs * 1e9) else "hbm"

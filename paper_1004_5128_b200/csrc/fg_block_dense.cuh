@@ -134,7 +134,7 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 #define FG_DENSE_SOLO 1   // large-field BT = 32 main launches: one 128-register CTA per SM (0: two 96-register CTAs)
 #endif
 #ifndef FG_DENSE_TAIL_RED
-#define FG_DENSE_TAIL_RED 0
+#define FG_DENSE_TAIL_RED 1   // accumulating launches add their tile into P with L2 reductions (0: load-add-store)
 #endif
 #ifndef FG_SOLO_FOLD
 #define FG_SOLO_FOLD 0
