@@ -146,7 +146,9 @@ def default_tblock(p: "Problem | None" = None) -> int:
     # give the full schedule's bits (reference property, test_covering_strategies)
     truncating = p.kind == "short" and short_horizon(p.param, float(p.dt[0])) < int(p.n_steps)
     if truncating:
-        return 24
+        # large single fields: 32, the solo dense main launch (c3-short 240 -> 231 ms,
+        # 220 ms with sub-blocks of 8, default_subblock); 24 measured best otherwise
+        return 32 if large_field(p) else 24
     # thinned schedules: the itemized block stage does work proportional to the
     # schedule's terms, so a wider block (fewer history passes) pays off up to
     # 56 (c2, one box: 35.8 ms at 40, 33.5 at 48, 32.7 at 56, 33.3 at 64 and 72 —
@@ -196,7 +198,8 @@ def default_subblock(p: "Problem", tblock: int) -> int:
         # dense schedules (one field): every step sums all its recent offsets,
         # so even short sub-blocks pay (c3-short 278 -> 262 ms at S = 4,
         # c3-full 693 -> 675 and c4-full 1414 -> 1370 at S = 8)
-        s = (8 if p.kind == "full" else 4) if large_field(p) and p.batch == 1 else 0
+        # (c3-short at tblock 32, S/D: 4/4 231-235, 8/8 231, 8/4 220, 8/2 225 ms)
+        s = (8 if p.kind == "full" or tblock == 32 else 4) if large_field(p) and p.batch == 1 else 0
     else:
         s = tblock // 4 if large_field(p) and tblock >= 112 else 0
     if s and (tblock % s or tblock // s > 16 or s < 2):
@@ -219,6 +222,8 @@ def default_subdelay(p: "Problem", subblock: int) -> int:
         # fewer recent slices.  Short memory (S = 4) keeps D = S (c3-short 247 vs
         # 267 at D = 2).
         d = subblock // 4
+    elif subblock == 8:
+        d = 4  # short memory at tblock 32 (see default_subblock)
     else:
         d = 0
     return d if 0 <= d <= subblock else 0

@@ -907,7 +907,12 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
     ++g_launches;
-    v.kern<<<block_grid(p, a.total_tiles), v.threads, v.smem, st>>>(a);
+#ifndef FG_TAIL_PER_SM
+#define FG_TAIL_PER_SM 2
+#endif
+    // beside a solo main launch: FG_TAIL_PER_SM = 1 leaves the main CTA room to start with the tail
+    const int tail_per_sm = choose_block_variant(p).per_sm == 1 ? FG_TAIL_PER_SM : 2;
+    v.kern<<<block_grid(p, a.total_tiles, tail_per_sm), v.threads, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
 
