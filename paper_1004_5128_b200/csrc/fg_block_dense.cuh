@@ -133,18 +133,6 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 #ifndef FG_DENSE_SOLO
 #define FG_DENSE_SOLO 1   // large-field BT = 32 main launches: one 128-register CTA per SM (0: two 96-register CTAs)
 #endif
-#ifndef FG_DENSE_TAIL_RED
-#define FG_DENSE_TAIL_RED 1   // accumulating launches add their tile into P with L2 reductions (0: load-add-store)
-#endif
-#ifndef FG_SOLO_FOLD
-#define FG_SOLO_FOLD 0
-#endif
-#ifndef FG_SOLO_LB
-#define FG_SOLO_LB 0
-#endif
-#ifndef FG_SOLO_REGS
-#define FG_SOLO_REGS 128
-#endif
 constexpr int kSoloStages = 4;  // ring of the solo main launch: 4 stages of 16 slices (two CTAs: 3)
 template <bool STAGED>
 __host__ __device__ constexpr int ring_stages() { return STAGED ? FG_STAGED_RING : 4; }
@@ -279,40 +267,7 @@ __device__ __forceinline__ void fg_block_tma_body(const BlockArgs& a) {
         nseg[tid] = fg_segments(a.kind, a.kb0 + tid, a.base, hz, segs + tid * kBlkSegs, kBlkSegs);
     __syncthreads();
 
-    // FOLD (solo launches): no producer warp — consumer warp 0 issues stage g-1+kStages
-    // after its third k-step of stage g, when every warp has released stage g-1's
-    // slot, so the CTA is 8 warps (two per SM sub-partition) and two step CTAs fit
-    // beside it instead of one
-    constexpr bool FOLD = SOLO && FG_SOLO_FOLD;
-    const uint64_t fold_pol = FOLD ? l2_evict_first_policy() : 0;
-    auto produce = [&](int64_t pg) {  // whole warp 0; stage pg of the CTA's tile sequence
-        if (n_st == 0) return;
-        const int64_t ti = pg / n_st, gl = pg - ti * n_st;
-        const int64_t tile = blockIdx.x + ti * gridDim.x;
-        if (tile >= a.total_tiles) return;
-        const int s = (int)(pg % kStages);
-        const int64_t q0 = (tile % a.tpm) * TP;
-        const int64_t row_elems = (a.ms - q0) < TP ? (a.ms - q0) : TP;
-        const uint32_t row_bytes = (uint32_t)(row_elems * sizeof(double));
-        const double* src0 = a.H + mem * a.ms + q0;
-        const int64_t t0 = ts + gl * KE;
-        const int nr = (int)((te - t0) < KE ? (te - t0) : KE);
-        const uint32_t cbytes = staged ? (uint32_t)(nr * CP * sizeof(double)) : 0u;
-        if (lane == 0) {
-            if (pg >= kStages) mbar_wait(&empty[s], (uint32_t)(((pg / kStages) & 1) ^ 1));
-            FG_DCHECK(t0 >= 0 && t0 + nr <= a.h_alloc && t0 + nr <= a.kb0);
-            mbar_expect_tx(&full[s], (uint32_t)nr * row_bytes + cbytes);
-        }
-        __syncwarp();
-        if (lane < nr)
-            bulk_g2s_hint(rows + ((size_t)s * KE + lane) * RP, src0 + (t0 + lane) * a.slice_stride, row_bytes, &full[s],
-                          fold_pol);
-        if (staged && lane == 31) bulk_g2s(coef + (size_t)s * KE * CP, a.gcoef + (t0 - ts) * CP, cbytes, &full[s]);
-    };
-    if (FOLD && warp == 0)
-        for (int pg = 0; pg < kStages; ++pg) produce(pg);
-
-    if (!FOLD && warp == NW) {  // ---- producer warp: lane 0 waits and arms the barrier, lane e copies row e
+    if (warp == NW) {  // ---- producer warp: lane 0 waits and arms the barrier, lane e copies row e
         // (one warp instruction issues a stage's row copies: c4-full 1292 -> 1285 ms)
         const uint64_t pol = l2_evict_first_policy();
         int64_t g = 0;  // stage counter over all tiles of the CTA
@@ -428,7 +383,6 @@ __device__ __forceinline__ void fg_block_tma_body(const BlockArgs& a) {
             for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[cur][i], bf[cur][j]);
-            if (FOLD && ks == 2 && warp == 0 && g >= 1) produce(g - 1 + kStages);
         }
         } else {
 #pragma unroll 1
@@ -489,15 +443,10 @@ __device__ __forceinline__ void fg_block_tma_body(const BlockArgs& a) {
             if (q >= a.n_m) continue;
             double* o = pout + bb * a.slice_stride + 8 * j;
             if (a.accumulate) {
-#if FG_DENSE_TAIL_RED
                 // one add per element and launch: an L2 reduction rounds exactly like
                 // load-add-store and spares the consumer warp the load round trip
                 red_add(o, d[i][j][0]);
                 red_add(o + 1, d[i][j][1]);
-#else
-                const double2 old = ld_cg2(o);
-                st_pair(o, __dadd_rn(old.x, d[i][j][0]), __dadd_rn(old.y, d[i][j][1]));
-#endif
             } else {
                 st_pair(o, d[i][j][0], d[i][j][1]);
             }
@@ -518,11 +467,7 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
 // DMMAs without waiting for shared memory; the second CTA's registers are left
 // to a step CTA of the block running beside it.
 template <int BT, int TP, bool STAGED, int NS, int WP>
-#if FG_SOLO_LB
-__global__ void __launch_bounds__(TP / WP * 32 + 32, 1) fg_block_tma_solo_kernel(const BlockArgs a) {
-#else
-__global__ void __maxnreg__(FG_SOLO_REGS) fg_block_tma_solo_kernel(const BlockArgs a) {
-#endif
+__global__ void __maxnreg__(128) fg_block_tma_solo_kernel(const BlockArgs a) {
     fg_block_tma_body<BT, TP, STAGED, NS, WP, true>(a);
 }
 

@@ -392,7 +392,7 @@ BlockVariant choose_block_variant(const fg_plan* p, bool tail = false) {
     // (one CTA per SM, fg_block_tma_solo_kernel) once every SM has several tiles
     if (FG_DENSE_SOLO && !tail && staged && p->tblock == 32 && (p->n_m + 255) / 256 >= 4 * (int64_t)sm_count()) {
         BlockVariant v = {fg_block_tma_solo_kernel<32, 256, true, kSoloStages, 32>,
-                          tma_block_smem<32, 256, true, kSoloStages, 32>(), 256, 256 / 32 * 32 + (FG_SOLO_FOLD ? 0 : 32)};
+                          tma_block_smem<32, 256, true, kSoloStages, 32>(), 256, 256 / 32 * 32 + 32};
         v.per_sm = 1;
         return v;
     }
@@ -907,12 +907,7 @@ int launch_block_tail(const fg_plan* p, int64_t kb0, int bt, cudaStream_t st) {
         return rc;
     if (int rc = prefer_max_smem((const void*)v.kern)) return rc;
     ++g_launches;
-#ifndef FG_TAIL_PER_SM
-#define FG_TAIL_PER_SM 2
-#endif
-    // beside a solo main launch: FG_TAIL_PER_SM = 1 leaves the main CTA room to start with the tail
-    const int tail_per_sm = choose_block_variant(p).per_sm == 1 ? FG_TAIL_PER_SM : 2;
-    v.kern<<<block_grid(p, a.total_tiles, tail_per_sm), v.threads, v.smem, st>>>(a);
+    v.kern<<<block_grid(p, a.total_tiles), v.threads, v.smem, st>>>(a);
     return cuda_check(cudaGetLastError(), "fg_block_tma tail launch");
 }
 

@@ -7,4 +7,4 @@ mkdir -p $OUT
 export FGB200_LIB=paper_1004_5128_b200/_lib/variants/libfgb200_checked.so
 timeout 3000 python -m pytest tests -q -m gpu -p no:cacheprovider > $OUT/pytest_checked.log 2>&1
 echo "checked suite rc=$?"; tail -3 $OUT/pytest_checked.log
-grep -c "FG_CHECK failed" $OUT/pytest_checked.log
+grep -c "FG_CHECK failed" $OUT/pytest_checked.log || true
