@@ -67,6 +67,42 @@ def test_block_partials_match_numpy(cuda_device, shape, kind, param, kb0, bt):
     assert np.abs(got - want).max() <= 1e-12 * max(scale, 1.0)
 
 
+@pytest.mark.parametrize("kind,param", [("full", 0), ("short", 300.0)])
+@pytest.mark.parametrize("kb0,bt", [(999, 32), (130, 32), (64, 32), (96, 32), (700, 17)])
+def test_solo_main_launch_matches_numpy(cuda_device, kind, param, kb0, bt):
+    """Large single fields at tblock 32 take the solo dense main launch (one CTA
+    per SM, software-pipelined fragments, 4-stage ring): ragged last tile (801
+    tiles of 256 points, several per CTA), fewer stages than the ring, partial
+    last stages and a short last block, against NumPy; reruns bitwise equal."""
+    import torch
+
+    import paper_1004_5128_b200 as fg
+    from paper_1004_5128_b200 import _lib
+    from paper_1004_5128_b200._engine import Stepper
+
+    shape = (401, 511)
+    n = int(np.prod(shape))
+    assert -(-n // 256) >= 4 * 148  # the library's solo threshold on a B200
+    strat = fg.FullMemory() if kind == "full" else fg.ShortMemory(param)
+    cfg = fg.FieldConfig(initial=np.zeros(shape), dx=1.0, gamma=0.63, dt=1.0, n_steps=kb0 + bt + 1, strategy=strat,
+                         history_byte_cap=None)
+    st = Stepper(cfg.to_problem(), tblock=32)
+    gen = torch.Generator(device=st.device).manual_seed(kb0 + bt)
+    st.H.copy_(torch.randn(st.H.shape, generator=gen, device=st.device, dtype=torch.float64))
+    L = _lib.load()
+    _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
+    torch.cuda.synchronize()
+    P1 = st.block_partials(kb0)[:bt].clone()
+    for rep in range(3):
+        _lib.check(L.fg_block_partials(C.byref(st.plan), kb0, bt, _lib.stream_handle()))
+        torch.cuda.synchronize()
+        assert torch.equal(P1, st.block_partials(kb0)[:bt]), f"rerun {rep} differs"
+    H = st.H[:kb0, :n].cpu().numpy()
+    want = expected_partials(H, kind, param, kb0, bt, st.psi[0].cpu().numpy())
+    got = P1[:, :n].cpu().numpy()
+    assert np.abs(got - want).max() <= 1e-12 * max(np.abs(want).max(), 1.0)
+
+
 @pytest.mark.parametrize("n_pts,B", [(300, 5), (512, 3), (40, 9)])
 @pytest.mark.parametrize("kb0,bt", [(16, 16), (160, 16), (1032, 24), (992, 32), (1008, 48), (1280, 64), (2000, 7), (1920, 128)])
 def test_ensemble_block_partials_match_numpy(cuda_device, n_pts, B, kb0, bt):
