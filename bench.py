@@ -440,6 +440,41 @@ def quick_line(name: str, rank: int, dev, args, stream, reps: int = 2) -> dict:
     return out
 
 
+def single_pass_step(dev, stream, peak_gbs: float, k_first: int = 1500, n_timed: int = 5) -> dict:
+    """The unblocked fused step kernel alone (tblock 0: ONE fg_step_kernel launch per
+    step streams every slice of the step's schedule from HBM, then stencil, reaction
+    and update in the same pass — the single-pass algorithm of the reference and of
+    BASELINE.json's north star): c4-full steps k_first .. k_first+n_timed-1, each timed
+    with CUDA events on the launching stream after an unblocked prefix has written the
+    history.  Algorithmic bytes of step k: its k+1 history slices, the field read and
+    the field and stencil slice written."""
+    import torch
+    from dataclasses import replace
+
+    from paper_1004_5128_b200._engine import Stepper
+
+    cfg = replace(workload("c4-full")[0], n_steps=k_first + n_timed)
+    st = Stepper(cfg.to_problem(), tblock=0)
+    st.advance(k_first)
+    torch.cuda.synchronize(dev)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_timed + 1)]
+    evs[0].record(stream)
+    for i in range(n_timed):
+        st.advance(k_first + i + 1)
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    st.raise_if_diverged()
+    us = [evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(n_timed)]
+    n = int(np.prod(cfg.to_problem().shape))
+    by = [(k_first + i + 1 + 3) * n * 8 for i in range(n_timed)]
+    gbs = sum(by) / (sum(us) * 1e-6) / 1e9
+    return {"kernel": "fg_step_kernel<3, saturating, 1, unblocked> (one launch per step, whole schedule streamed)",
+            "workload": f"c4-full steps {k_first}..{k_first + n_timed - 1} with temporal blocking off",
+            "us_per_step": us, "algorithmic_bytes_per_step": by, "bound": "hbm", "achieved": gbs, "peak": peak_gbs,
+            "unit": "GB/s", "frac": gbs / peak_gbs,
+            "ncu": "profiles/r02n_unblocked_c4f_step_ncu_full.txt (DRAM bytes 1.00x algorithmic)"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -572,6 +607,13 @@ def run_ours(args) -> None:
             except Exception as exc:  # the headline line must survive a failed side measurement
                 others[name] = {"error": f"{type(exc).__name__}: {exc}"}
         torch.cuda.empty_cache()
+    single = None
+    if others is not None:
+        try:
+            single = single_pass_step(dev, stream, peak)
+        except Exception as exc:
+            single = {"error": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -600,6 +642,7 @@ def run_ours(args) -> None:
                     "seconds_per_step": e2e_max},
             "clocks": clocks,
             "other_configs": others,
+            "single_pass_step": single,
             "per_step_ms": per_step_ms,
             "device": torch.cuda.get_device_name(dev),
         }
