@@ -124,7 +124,8 @@ def default_tblock(p: "Problem | None" = None) -> int:
     Measured on B200 (profiles/r01_summary.md, tblock sweep): single-member
     full memory at 32 (the dense block kernel turns fp64-tensor bound);
     adaptive at 128 with 16-column items for large fields (c3, c4, c5) and at
-    56 with 8-column items otherwise (c2); short memory and other ensembles
+    56 with 8-column items otherwise (c2); short memory on large single fields
+    at 32 too (the solo dense main launch), other short memory and ensembles
     (per-member tables built in the CTA) at 24.
     """
     env = os.environ.get("FGB200_TBLOCK")
