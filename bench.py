@@ -255,6 +255,10 @@ def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # torchrun pins OMP_NUM_THREADS=1 for every rank; only rank 0 works here, so it
+        # takes every host core it may run on (set before the oracle library loads libgomp)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     for run in runs_of(args.config):  # warm (page cache, OpenMP pool)
         cpu_reference(workload(run)[0], REF_WARM_STEPS)
     tot_terms, tot_time, what = 0, 0.0, ""
