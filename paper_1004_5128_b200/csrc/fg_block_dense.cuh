@@ -131,7 +131,7 @@ __host__ __device__ constexpr int coef_pitch() { return BT + 4; }
 #define FG_TAIL_STAGES 2
 #endif
 #ifndef FG_DENSE_SOLO
-#define FG_DENSE_SOLO 1   // large-field BT = 32 main launches: one 128-register CTA per SM (0: two 96-register CTAs)
+#define FG_DENSE_SOLO 1   // large-field BT = 32 main launches: one CTA per SM, <= 128 registers (0: two 96-register CTAs)
 #endif
 constexpr int kSoloStages = 4;  // ring of the solo main launch: 4 stages of 16 slices (two CTAs: 3)
 template <bool STAGED>
@@ -356,7 +356,7 @@ __device__ __forceinline__ void fg_block_tma_body(const BlockArgs& a) {
         // DMMA (c4-full 1310 -> 1277 ms, c3-full 633 -> 616)
         if constexpr (SOLO) {
         // fragments of k-step ks+1 are loaded before the DMMAs of k-step ks issue
-        // (two k-steps live, 112 registers): the shared-memory latency hides
+        // (two k-steps live, 110 registers, no spills): the shared-memory latency hides
         // behind the warp's own 16 DMMAs instead of behind other warps
         double af[2][MT], bf[2][NT];
 #pragma unroll
@@ -461,8 +461,8 @@ __global__ void __launch_bounds__(TP / WP * 32 + 32, 2) fg_block_tma_kernel(cons
     fg_block_tma_body<BT, TP, STAGED, NS, WP, false>(a);
 }
 
-// "Solo" main launch of large single fields at BT = 32: ONE CTA per SM with 128
-// registers per thread, so the lean consumer loop can keep two k-steps of
+// "Solo" main launch of large single fields at BT = 32: ONE CTA per SM with up to
+// 128 registers per thread (ptxas: 110), so the lean consumer loop can keep two k-steps of
 // fragments live (software-pipelined, no spills) and the 8 consumer warps issue
 // DMMAs without waiting for shared memory; the second CTA's registers are left
 // to a step CTA of the block running beside it.
