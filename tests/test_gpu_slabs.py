@@ -74,6 +74,7 @@ def test_slab_two_ranks_one_gpu_gloo(cuda_device):
     cuda:0, every rank runs the engine on its slab, edge rows travel over gloo
     through the host.  Same layout, plan and gather as the NCCL run."""
     env = dict(os.environ, FGB200_SLAB_TEST_BACKEND="gloo")
+    env.setdefault("GLOO_SOCKET_IFNAME", "lo")  # both ranks are local; the box's hostname may not resolve
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29534", os.path.abspath(__file__)]
     res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
